@@ -1,0 +1,176 @@
+/*
+ * fscnn_b200.h -- C ABI of the B200-native FSCNN sparse-convolution path.
+ *
+ * Drop-in boundary for the reference package sparse_infer (FSCNN, arXiv 2212.08815).
+ * The reference has no native FFI: its operator API is the Python function surface
+ * re-exported by sparse_infer/__init__.py:9-74, and each Python wrapper hands flat
+ * numpy arrays to one numba kernel.  Every entry point below replaces one of those
+ * kernel calls (cited per function) with a stream-ordered launch over DEVICE
+ * pointers; INTEGRATION.md shows the ctypes binding a sparse_infer maintainer adds.
+ *
+ * Conventions (all entry points):
+ *   - Pointers are CUDA device pointers; sizes are element counts; strides are in
+ *     elements.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Node buffers are arrays of fscnn_node, byte-identical to the reference's
+ *     NODE_DTYPE = [("index","<i4"),("value","<f4")] (sparse_core.py:24); a node
+ *     with index -1 is a segment sentinel with value +0.0.  Offset tables are int64
+ *     (sparse_core.py:321-323).
+ *   - Dense activations on the device are NCHW float32 ([N][C][H][W]).  The
+ *     reference's channel-innermost (W,H,C) DenseTensor3 layout (sparse_core.py:9-13)
+ *     is converted at the boundary by fscnn_whc_to_nchw / fscnn_nchw_to_whc.
+ *   - Return value: FSCNN_OK or an error code; fscnn_last_error() describes the
+ *     last failure on the calling thread.  Validation of shapes and formats is the
+ *     caller's (Python) job, as in the reference (kernels are unchecked there too);
+ *     the ABI checks only what would make a launch unsafe.
+ *   - All kernels are deterministic: results never depend on launch configuration,
+ *     batch position or device count (reference contract layers.py:149-155).
+ */
+#ifndef FSCNN_B200_H
+#define FSCNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fscnn_node {
+    int32_t index; /* coordinate along the innermost stored axis; -1 = sentinel */
+    float value;
+} fscnn_node;
+
+enum fscnn_status {
+    FSCNN_OK = 0,
+    FSCNN_ERR_ARG = 1,         /* bad argument (null pointer, negative extent, ...) */
+    FSCNN_ERR_CUDA = 2,        /* a CUDA runtime call or launch failed */
+    FSCNN_ERR_UNSUPPORTED = 3  /* geometry not handled by the requested kernel */
+};
+
+/* Library identity / diagnostics. */
+int fscnn_abi_version(void);
+const char *fscnn_last_error(void);
+/* Number of kernel launches this library issued since the last reset (host-side counter). */
+int64_t fscnn_launch_count(void);
+void fscnn_reset_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Encoder: dense -> node format.
+ * Replaces sparsify_tensor3 (sparse_core.py:334-353) with _build_segmented
+ * (sparse_core.py:319-331), batched the way SparseTensor4.stack concatenates
+ * tensors (sparse_core.py:273-290).
+ *
+ * The source is viewed as `batch` tensors, each arranged (outer, mid, inner) for
+ * the requested axis order; element (b, o, m, i) lives at
+ *   src[b*s_b + o*s_o + m*s_m + i*s_i].
+ * Segment s = (b*outer + o)*mid + m holds the nonzeros (v != 0.0f: -0.0 dropped,
+ * NaN kept) of its inner fiber in ascending i, then one sentinel.
+ * seg_off[s] = sum_{t<s} (count[t] + 1)  -- the reference's global offsets.
+ *
+ * Two calls: fscnn_encode_offsets fills seg_off and *total_nodes (device scalar),
+ * the caller sizes the node buffer, then fscnn_encode_nodes writes it.
+ * matrix_off (batch*outer, = seg_off[::mid]) and tensor_off (batch) may be NULL.
+ * ------------------------------------------------------------------------- */
+size_t fscnn_encode_workspace_bytes(int64_t n_segments);
+int fscnn_encode_offsets(const float *src, int64_t batch, int64_t outer, int64_t mid,
+                         int64_t inner, int64_t s_b, int64_t s_o, int64_t s_m, int64_t s_i,
+                         int64_t *seg_off, int64_t *total_nodes, void *workspace,
+                         size_t workspace_bytes, void *stream);
+int fscnn_encode_nodes(const float *src, int64_t batch, int64_t outer, int64_t mid,
+                       int64_t inner, int64_t s_b, int64_t s_o, int64_t s_m, int64_t s_i,
+                       const int64_t *seg_off, fscnn_node *nodes, int64_t *matrix_off,
+                       int64_t *tensor_off, void *stream);
+
+/* Decoder: node format -> dense.  Replaces densify_tensor3 (sparse_core.py:356-368).
+ * Writes every element of the strided destination view (zeros where no node). */
+int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch, int64_t outer,
+                 int64_t mid, int64_t inner, float *dst, int64_t d_b, int64_t d_o, int64_t d_m,
+                 int64_t d_i, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Sparse-Filter convolution, reference order (bit-exact).
+ * Replaces _conv_all_filters_kernel (layers.py:170-180) / _conv_filter_sparse_kernel
+ * (kernels.py:100-105) over _window_acc (kernels.py:78-97): for every output,
+ * taps kw outer, kh inner, nodes ascending c, separate fp32 multiply and add, then
+ * + bias[k].  Any geometry (h_f, w_f, stride >= 1, pad >= 0).
+ *   x: [n][c][h][w]; nodes/seg_off: CHW SparseTensor4 of K filters, seg_off
+ *   [K][w_f*h_f] global; y: [n][K][n_h][n_w]; bias may be NULL (adds +0.0).
+ *   relu != 0 applies np.maximum(y, 0) semantics to the result.
+ * ------------------------------------------------------------------------- */
+int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_node *nodes,
+                        const int64_t *seg_off, int k, int h_f, int w_f, int stride, int pad,
+                        const float *bias, int relu, float *y, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Sparse-Filter convolution, fast path (3x3, stride 1, pad 1 -- every VGG16 conv).
+ * Same result as fscnn_sf_conv_exact up to fp32 reassociation (channel-major
+ * accumulation order).  Consumes the kernel-side packed filter stream:
+ *   the filter bank regrouped into groups of `kt` filters; for group g and input
+ *   channel c, segment g*c_n + c lists the nonzeros W[g*kt + kl][c][kh][kw] as
+ *   nodes with index = kl*9 + kh*3 + kw, ascending, sentinel-terminated.
+ * Build it with fscnn_sf_pack_offsets / fscnn_sf_pack_nodes from a dense
+ * [K][C][3][3] bank (itself decoded from the reference's CHW SparseTensor4 by
+ * fscnn_decode, or straight from dense weights).
+ * ------------------------------------------------------------------------- */
+int fscnn_sf_pack_kt(void); /* filters per group the fast kernel expects */
+int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int64_t *seg_off,
+                          int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                          void *stream);
+int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, const int64_t *seg_off,
+                        fscnn_node *nodes, void *stream);
+/* Fast conv.  x: [n][c][h][ldi] (ldi >= w, ldi % 4 == 0, 16-byte aligned; the
+ * columns w..ldi-1 are never read).  y: [n][k][h][ldo], or with pool != 0 the fused
+ * 2x2 max-pool result [n][k][h/2][ldo].  packed/packed_seg_off/total_nodes: the
+ * packed stream (allocate total_nodes + 2 nodes: the kernel bulk-copies 16-byte
+ * aligned ranges).  max_chunk_entries: the largest node count (sentinels included)
+ * of any group over any run of `cc` consecutive channels.  ly selects the
+ * sub-region height 4*ly (8, 4 or 2; 0 = by h).  relu applies np.maximum(.,0)
+ * before the pool, as the reference's conv -> relu -> pool sequence does. */
+int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
+                        const fscnn_node *packed, const int64_t *packed_seg_off,
+                        int64_t total_nodes, int max_chunk_entries, int cc, int k,
+                        const float *bias, int relu, int pool, float *y, int ldo, int ly,
+                        void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Sparse-Input convolution (bit-exact).
+ * Replaces _conv_input_sparse_kernel (kernels.py:136-166) for all K filters at once:
+ * output (i,j) of filter k sums, kw outer, kh inner, over the input fiber nodes at
+ * (w_in, h_in) ascending c, filt[k][c][kh][kw] * v.  Results that compare equal to
+ * 0.0 are written as +0.0 (the reference stores no node for them).
+ *   in_nodes: CHW node buffer of n images; in_seg_off: [n][w*h] global offsets
+ *   (segment (w_in*h + h_in)); wt: dense filters transposed to [c][kh][kw][K]
+ *   (see fscnn_kcrs_to_crsk); y: [n][K][n_h][n_w] (+ bias[k] if bias != NULL).
+ * ------------------------------------------------------------------------- */
+int fscnn_si_conv(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
+                  int w, const float *wt, int k, int h_f, int w_f, int stride, int pad,
+                  const float *bias, float *y, void *stream);
+int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w_crsk,
+                       void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Dense layers between convolutions.
+ *   fscnn_relu: np.maximum(x, 0) semantics (layers.py:469-484): NaN propagates,
+ *     -0.0 -> +0.0.
+ *   fscnn_pool2d: _pool_dense_kernel (layers.py:250-271) on NCHW: non-overlapping
+ *     (h_p, w_p) windows; max: -inf start, take v iff v > acc (ph outer, pw inner);
+ *     avg: same-order sum / (h_p*w_p).
+ *   Layout converters between the reference's (W,H,C) DenseTensor3 memory and NCHW.
+ * ------------------------------------------------------------------------- */
+int fscnn_relu(const float *x, int64_t count, float *y, void *stream);
+int fscnn_pool2d(const float *x, int n, int c, int h, int w, int h_p, int w_p, int use_max,
+                 float *y, void *stream);
+int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_nchw,
+                      void *stream);
+int fscnn_nchw_to_whc(const float *x_nchw, int n, int c, int h, int w, float *y_whc,
+                      void *stream);
+
+/* FP32 CUDA-core throughput probe (roofline denominator): `blocks` x 256 threads,
+ * each 8 independent FFMA chains of 16*iters steps = 256*blocks*iters*256 FLOPs. */
+int fscnn_fp32_probe(float *out, int blocks, int iters, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSCNN_B200_H */

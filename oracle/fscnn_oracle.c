@@ -119,7 +119,7 @@ void oracle_decode(const node_t *nodes, const int64_t *seg_off, int64_t n_seg, i
  * Padding is virtual (out-of-range taps skipped).  Input and output are the
  * reference's channel-innermost (W, H, C) layout, one image after another.
  * seg_off is the SparseTensor4 global segment table (K x H_F*W_F, int64).
- * Parallel over (image, output column) -- results do not depend on threads.
+ * Parallel over (image, output column, output row) -- results do not depend on threads.
  * ------------------------------------------------------------------------- */
 static float window_acc(const float *inp, int h_i, int w_i, int c_n, const node_t *nodes,
                         const int64_t *seg_off, int64_t seg_base, int w_f, int h_f, int w0,
@@ -152,12 +152,12 @@ void oracle_sf_conv(const float *inp, int64_t n_img, int c_n, int h_i, int w_i,
     int64_t in_sz = (int64_t)c_n * h_i * w_i;
     int64_t out_sz = (int64_t)k_n * n_h * n_w;
     set_threads(n_threads);
-#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+#pragma omp parallel for collapse(3) schedule(dynamic, 4)
     for (int64_t img = 0; img < n_img; ++img)
-        for (int w = 0; w < n_w; ++w) {
-            const float *in_img = inp + img * in_sz;
-            float *o = out + img * out_sz;
-            for (int h = 0; h < n_h; ++h)
+        for (int w = 0; w < n_w; ++w)
+            for (int h = 0; h < n_h; ++h) {
+                const float *in_img = inp + img * in_sz;
+                float *o = out + img * out_sz;
                 for (int f = 0; f < k_n; ++f) {
                     float x = window_acc(in_img, h_i, w_i, c_n, nodes, seg_off,
                                          (int64_t)f * h_f * w_f, w_f, h_f, w * stride - pad,

@@ -1,0 +1,210 @@
+// Memory-bound layers between convolutions and layout converters.
+//   relu      -- np.maximum(x, 0) (layers.py:469-484)
+//   pool2d    -- _pool_dense_kernel (layers.py:250-271) on NCHW
+//   whc<->nchw -- DenseTensor3 memory (sparse_core.py:9-13) <-> device NCHW
+//   kcrs->crsk -- dense filter bank transposed for the sparse-input kernel
+// All are HBM-bound streaming kernels: grid-stride, float4 where aligned.
+#include "common.cuh"
+
+namespace fscnn {
+namespace {
+
+template <bool VEC>
+__global__ void relu_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ y) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t head = 0;
+    if (VEC) {
+        int64_t n4 = n >> 2;
+        const float4 *x4 = reinterpret_cast<const float4 *>(x);
+        float4 *y4 = reinterpret_cast<float4 *>(y);
+        for (int64_t i = t0; i < n4; i += stride) {
+            float4 v = x4[i];
+            v.x = relu_np(v.x);
+            v.y = relu_np(v.y);
+            v.z = relu_np(v.z);
+            v.w = relu_np(v.w);
+            y4[i] = v;
+        }
+        head = n4 << 2;
+    }
+    for (int64_t i = head + t0; i < n; i += stride) y[i] = relu_np(x[i]);
+}
+
+// One thread per output element (n, c, ho, wo); reads the window rows (ph outer, pw inner).
+__global__ void pool2d_kernel(const float *__restrict__ x, int64_t total, int h, int w, int h_p,
+                              int w_p, int use_max, float *__restrict__ y) {
+    int h_o = h / h_p, w_o = w / w_p;
+    float area = (float)(h_p * w_p);
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        int wo = (int)(t % w_o);
+        int64_t r = t / w_o;
+        int ho = (int)(r % h_o);
+        int64_t nc = r / h_o;
+        const float *src = x + nc * h * (int64_t)w + (int64_t)(ho * h_p) * w + wo * w_p;
+        float acc = use_max ? -INFINITY : 0.0f;
+        for (int ph = 0; ph < h_p; ++ph)
+            for (int pw = 0; pw < w_p; ++pw) {
+                float v = src[(int64_t)ph * w + pw];
+                if (use_max) {
+                    if (v > acc) acc = v;
+                } else {
+                    acc = __fadd_rn(acc, v);
+                }
+            }
+        y[t] = use_max ? acc : __fdiv_rn(acc, area);
+    }
+}
+
+// Specialised 2x2 max-pool (every VGG16 pool): float2 row reads, same -inf / '>' rule.
+__global__ void maxpool2x2_kernel(const float *__restrict__ x, int64_t total, int h, int w,
+                                  float *__restrict__ y) {
+    int h_o = h >> 1, w_o = w >> 1;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        int wo = (int)(t % w_o);
+        int64_t r = t / w_o;
+        int ho = (int)(r % h_o);
+        int64_t nc = r / h_o;
+        const float *src = x + nc * h * (int64_t)w + (int64_t)(2 * ho) * w + 2 * wo;
+        float2 a = *reinterpret_cast<const float2 *>(src);
+        float2 b = *reinterpret_cast<const float2 *>(src + w);
+        float acc = -INFINITY;
+        if (a.x > acc) acc = a.x;
+        if (a.y > acc) acc = a.y;
+        if (b.x > acc) acc = b.x;
+        if (b.y > acc) acc = b.y;
+        y[t] = acc;
+    }
+}
+
+// (W,H,C)-memory image -> NCHW, 32x32 smem transpose over (c, hw) per image.
+__global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
+                                   float *__restrict__ y) {
+    __shared__ float tile[32][33];
+    int img = blockIdx.z;
+    const float *src = x + (int64_t)img * c_n * hw;
+    float *dst = y + (int64_t)img * c_n * hw;
+    int c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;  // p = w*H + h in source order
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int p = p0 + j, c = c0 + threadIdx.x;
+        if (p < hw && c < c_n) tile[j][threadIdx.x] = src[(int64_t)p * c_n + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int c = c0 + j, p = p0 + threadIdx.x;
+        if (p < hw && c < c_n) {
+            int wi = p / h, hi = p % h;
+            dst[(int64_t)c * hw + (int64_t)hi * w + wi] = tile[threadIdx.x][j];
+        }
+    }
+}
+
+__global__ void nchw_to_whc_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
+                                   float *__restrict__ y) {
+    __shared__ float tile[32][33];
+    int img = blockIdx.z;
+    const float *src = x + (int64_t)img * c_n * hw;
+    float *dst = y + (int64_t)img * c_n * hw;
+    int c0 = blockIdx.y * 32, q0 = blockIdx.x * 32;  // q = h*W + w in source order
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int c = c0 + j, q = q0 + threadIdx.x;
+        if (q < hw && c < c_n) tile[j][threadIdx.x] = src[(int64_t)c * hw + q];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        int q = q0 + j, c = c0 + threadIdx.x;
+        if (q < hw && c < c_n) {
+            int hi = q / w, wi = q % w;
+            dst[((int64_t)wi * h + hi) * c_n + c] = tile[threadIdx.x][j];
+        }
+    }
+}
+
+__global__ void kcrs_to_crsk_kernel(const float *__restrict__ src, int k_n, int crs,
+                                    float *__restrict__ dst) {
+    int64_t total = (int64_t)k_n * crs;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        int k = (int)(t % k_n);
+        int64_t j = t / k_n;
+        dst[t] = src[(int64_t)k * crs + j];
+    }
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+    int64_t b = ceil_div(n, threads);
+    return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+}  // namespace fscnn
+
+using namespace fscnn;
+
+extern "C" {
+
+int fscnn_relu(const float *x, int64_t count, float *y, void *stream) {
+    FSCNN_REQUIRE(count >= 0 && (count == 0 || (x && y)), "bad relu arguments");
+    if (count == 0) return FSCNN_OK;
+    bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+    if (aligned)
+        relu_kernel<true><<<grid_for(count / 4 + 1, 256), 256, 0, as_stream(stream)>>>(x, count, y);
+    else
+        relu_kernel<false><<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(x, count, y);
+    FSCNN_LAUNCH_CHECK("relu_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_pool2d(const float *x, int n, int c, int h, int w, int h_p, int w_p, int use_max,
+                 float *y, void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    FSCNN_REQUIRE(h_p > 0 && w_p > 0, "pool window must be positive");
+    FSCNN_REQUIRE(h % h_p == 0 && w % w_p == 0, "input not divisible by pool window");
+    int64_t total = (int64_t)n * c * (h / h_p) * (w / w_p);
+    if (total == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && y, "null buffer");
+    bool even_rows = (w % 2 == 0) && ((reinterpret_cast<uintptr_t>(x) & 7) == 0);
+    if (use_max && h_p == 2 && w_p == 2 && even_rows) {
+        maxpool2x2_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(x, total, h, w, y);
+        FSCNN_LAUNCH_CHECK("maxpool2x2_kernel");
+    } else {
+        pool2d_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(x, total, h, w, h_p, w_p,
+                                                                          use_max, y);
+        FSCNN_LAUNCH_CHECK("pool2d_kernel");
+    }
+    return FSCNN_OK;
+}
+
+int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_nchw,
+                      void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
+    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
+    whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, y_nchw);
+    FSCNN_LAUNCH_CHECK("whc_to_nchw_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_nchw_to_whc(const float *x_nchw, int n, int c, int h, int w, float *y_whc,
+                      void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
+    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
+    nchw_to_whc_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_nchw, c, h * w, h, w, y_whc);
+    FSCNN_LAUNCH_CHECK("nchw_to_whc_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w_crsk,
+                       void *stream) {
+    FSCNN_REQUIRE(k > 0 && c > 0 && r > 0 && s > 0 && w_kcrs && w_crsk, "bad transpose arguments");
+    int64_t total = (int64_t)k * c * r * s;
+    kcrs_to_crsk_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(w_kcrs, k, c * r * s,
+                                                                            w_crsk);
+    FSCNN_LAUNCH_CHECK("kcrs_to_crsk_kernel");
+    return FSCNN_OK;
+}
+
+}  // extern "C"

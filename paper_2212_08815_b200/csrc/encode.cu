@@ -1,0 +1,359 @@
+// Dense <-> node-format conversion on the device, bit-exact with the reference
+// encoder (sparse_core.py:319-353, SparseTensor4.stack :273-290) and decoder
+// (densify_tensor3, sparse_core.py:356-368).
+//
+// Encoding is count -> exclusive scan of (count + 1) -> ordered write, exactly the
+// reference's bincount/cumsum/scatter, so offsets and node order match by
+// construction.  Two source walkers:
+//   * thread-per-segment: one thread scans one inner fiber (any stride); used when
+//     the inner axis is strided (e.g. CHW nodes from NCHW activations -- adjacent
+//     threads then read adjacent addresses of the mid axis... or stride-W rows);
+//   * warp-per-segment: a warp scans a contiguous fiber 32 values at a time and
+//     compacts with ballot/popc, preserving order.
+// The scan is a three-kernel block scan over int64 (4096 segments per block).
+#include "common.cuh"
+
+namespace fscnn {
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// --- source walkers ----------------------------------------------------------
+
+struct StridedSrc {
+    const float *p;
+    int64_t outer, mid, inner, s_b, s_o, s_m, s_i;
+    struct Fiber {
+        const float *p;
+    };
+    __device__ __forceinline__ Fiber fiber(int64_t s) const {
+        int64_t m = s % mid;
+        int64_t bo = s / mid;
+        int64_t o = bo % outer;
+        int64_t b = bo / outer;
+        return {p + b * s_b + o * s_o + m * s_m};
+    }
+    __device__ __forceinline__ float at(Fiber f, int64_t i) const { return f.p[i * s_i]; }
+};
+
+// Fast-path filter packing: segment s = g*C + c; inner i = kl*9 + tap reads
+// W[g*kt + kl][c][tap] from a dense [K][C][3][3] bank (zero past K).
+struct SfPackSrc {
+    const float *w;
+    int64_t k, c, kt;
+    int64_t inner;
+    struct Fiber {
+        const float *p;
+        int64_t kmax;
+    };
+    __device__ __forceinline__ Fiber fiber(int64_t s) const {
+        int64_t g = s / c, ch = s % c;
+        int64_t kmax = k - g * kt;
+        return {w + ((g * kt) * c + ch) * 9, kmax < kt ? kmax : kt};
+    }
+    __device__ __forceinline__ float at(Fiber f, int64_t i) const {
+        int64_t kl = i / 9, tap = i - kl * 9;
+        return kl < f.kmax ? f.p[kl * c * 9 + tap] : 0.0f;
+    }
+};
+
+template <class Src>
+__global__ void count_thread_kernel(Src src, int64_t n_seg, int64_t *cnt) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    auto b = src.fiber(s);
+    int64_t n = 0;
+    for (int64_t i = 0; i < src.inner; ++i) n += (src.at(b, i) != 0.0f);
+    cnt[s] = n + 1;
+}
+
+template <class Src>
+__global__ void count_warp_kernel(Src src, int64_t n_seg, int64_t *cnt) {
+    int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (s >= n_seg) return;
+    auto b = src.fiber(s);
+    int64_t n = 0;
+    for (int64_t i0 = 0; i0 < src.inner; i0 += 32) {
+        int64_t i = i0 + lane;
+        bool nz = (i < src.inner) && (src.at(b, i) != 0.0f);
+        n += __popc(__ballot_sync(0xffffffffu, nz));
+    }
+    if (lane == 0) cnt[s] = n + 1;
+}
+
+template <class Src>
+__global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    auto b = src.fiber(s);
+    int64_t p = seg_off[s];
+    for (int64_t i = 0; i < src.inner; ++i) {
+        float v = src.at(b, i);
+        if (v != 0.0f) nodes[p++] = make_int2((int)i, __float_as_int(v));
+    }
+    nodes[p] = make_int2(-1, 0);
+}
+
+template <class Src>
+__global__ void write_warp_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes) {
+    int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (s >= n_seg) return;
+    auto b = src.fiber(s);
+    int64_t p = seg_off[s];
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t i0 = 0; i0 < src.inner; i0 += 32) {
+        int64_t i = i0 + lane;
+        float v = (i < src.inner) ? src.at(b, i) : 0.0f;
+        bool nz = v != 0.0f;
+        unsigned m = __ballot_sync(0xffffffffu, nz);
+        if (nz) nodes[p + __popc(m & lt)] = make_int2((int)i, __float_as_int(v));
+        p += __popc(m);
+    }
+    if (lane == 0) nodes[p] = make_int2(-1, 0);
+}
+
+// --- int64 exclusive scan -------------------------------------------------------
+
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
+    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns exclusive prefix, *total = sum.
+__device__ int64_t block_excl_scan(int64_t v, int64_t *total) {
+    __shared__ int64_t warp_sums[32];
+    __shared__ int64_t block_total;
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t incl = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int nw = blockDim.x >> 5;
+        int64_t w = lane < nw ? warp_sums[lane] : 0;
+        int64_t wi = warp_incl_scan(w);
+        if (lane < nw) warp_sums[lane] = wi - w;
+        if (lane == nw - 1) block_total = wi;
+    }
+    __syncthreads();
+    int64_t excl = warp_sums[wid] + incl - v;
+    if (total) *total = block_total;
+    __syncthreads();
+    return excl;
+}
+
+__global__ void scan_tiles_kernel(int64_t *a, int64_t n, int64_t *tile_sums) {
+    int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * (int64_t)kScanItems;
+    int64_t v[kScanItems];
+    int64_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        v[j] = (base + j < n) ? a[base + j] : 0;
+        sum += v[j];
+    }
+    int64_t tot;
+    int64_t run = block_excl_scan(sum, &tot);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        if (base + j < n) a[base + j] = run;
+        run += v[j];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+// One block scans all tile sums (exclusive, in place); writes the grand total.
+__global__ void scan_sums_kernel(int64_t *sums, int64_t n, int64_t *total) {
+    int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    int64_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    int64_t s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += sums[i];
+    int64_t tot;
+    int64_t run = block_excl_scan(s, &tot);
+    for (int64_t i = lo; i < hi; ++i) {
+        int64_t t = sums[i];
+        sums[i] = run;
+        run += t;
+    }
+    if (threadIdx.x == 0) *total = tot;
+}
+
+__global__ void scan_add_kernel(int64_t *a, int64_t n, const int64_t *tile_sums) {
+    int64_t base = blockIdx.x * (int64_t)kScanTile;
+    int64_t add = tile_sums[blockIdx.x];
+    if (add == 0) return;
+    for (int j = threadIdx.x; j < kScanTile; j += blockDim.x)
+        if (base + j < n) a[base + j] += add;
+}
+
+__global__ void side_tables_kernel(const int64_t *seg_off, int64_t n_seg, int64_t mid,
+                                   int64_t per_tensor, int64_t *matrix_off, int64_t *tensor_off) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    if (matrix_off && s % mid == 0) matrix_off[s / mid] = seg_off[s];
+    if (tensor_off && s % per_tensor == 0) tensor_off[s / per_tensor] = seg_off[s];
+}
+
+int scan_inplace(int64_t *a, int64_t n, int64_t *total, void *ws, size_t ws_bytes,
+                 cudaStream_t st) {
+    int64_t tiles = ceil_div(n, kScanTile);
+    FSCNN_REQUIRE(ws_bytes >= (size_t)tiles * sizeof(int64_t) && ws != nullptr,
+                  "encode workspace too small (%zu bytes, need %lld)", ws_bytes,
+                  (long long)(tiles * 8));
+    int64_t *sums = static_cast<int64_t *>(ws);
+    scan_tiles_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(a, n, sums);
+    FSCNN_LAUNCH_CHECK("scan_tiles_kernel");
+    scan_sums_kernel<<<1, kScanThreads, 0, st>>>(sums, tiles, total);
+    FSCNN_LAUNCH_CHECK("scan_sums_kernel");
+    if (tiles > 1) {
+        scan_add_kernel<<<(unsigned)tiles, 256, 0, st>>>(a, n, sums);
+        FSCNN_LAUNCH_CHECK("scan_add_kernel");
+    }
+    return FSCNN_OK;
+}
+
+// Warp-per-segment pays off only when fibers are contiguous and long enough.
+inline bool use_warp_walker(int64_t inner, int64_t s_i) { return s_i == 1 && inner >= 32; }
+
+template <class Src>
+int encode_offsets_impl(const Src &src, int64_t n_seg, bool warp_mode, int64_t *seg_off,
+                        int64_t *total, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (n_seg == 0) {
+        cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+        return check_launch("memset total");
+    }
+    if (warp_mode) {
+        count_warp_kernel<<<(unsigned)ceil_div(n_seg * 32, 256), 256, 0, st>>>(src, n_seg, seg_off);
+        FSCNN_LAUNCH_CHECK("count_warp_kernel");
+    } else {
+        count_thread_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(src, n_seg, seg_off);
+        FSCNN_LAUNCH_CHECK("count_thread_kernel");
+    }
+    return scan_inplace(seg_off, n_seg, total, ws, ws_bytes, st);
+}
+
+template <class Src>
+int encode_nodes_impl(const Src &src, int64_t n_seg, bool warp_mode, const int64_t *seg_off,
+                      fscnn_node *nodes, cudaStream_t st) {
+    if (n_seg == 0) return FSCNN_OK;
+    int2 *out = reinterpret_cast<int2 *>(nodes);
+    if (warp_mode) {
+        write_warp_kernel<<<(unsigned)ceil_div(n_seg * 32, 256), 256, 0, st>>>(src, n_seg, seg_off, out);
+        FSCNN_LAUNCH_CHECK("write_warp_kernel");
+    } else {
+        write_thread_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(src, n_seg, seg_off, out);
+        FSCNN_LAUNCH_CHECK("write_thread_kernel");
+    }
+    return FSCNN_OK;
+}
+
+// --- decoder ----------------------------------------------------------------------
+
+__global__ void decode_kernel(const int2 *nodes, const int64_t *seg_off, int64_t n_seg,
+                              int64_t outer, int64_t mid, int64_t inner, float *dst, int64_t d_b,
+                              int64_t d_o, int64_t d_m, int64_t d_i) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    int64_t m = s % mid, bo = s / mid, o = bo % outer, b = bo / outer;
+    float *d = dst + b * d_b + o * d_o + m * d_m;
+    int64_t p = seg_off[s];
+    int2 nd = nodes[p];
+    for (int64_t i = 0; i < inner; ++i) {
+        float v = 0.0f;
+        if (nd.x == i) {
+            v = __int_as_float(nd.y);
+            nd = nodes[++p];
+        }
+        d[i * d_i] = v;
+    }
+}
+
+constexpr int kSfPackKt = 8;  // must match KT in sf_conv.cu
+
+}  // namespace
+
+}  // namespace fscnn
+
+using namespace fscnn;
+
+extern "C" {
+
+size_t fscnn_encode_workspace_bytes(int64_t n_segments) {
+    return (size_t)(ceil_div(n_segments > 0 ? n_segments : 1, kScanTile) + 1) * sizeof(int64_t);
+}
+
+int fscnn_encode_offsets(const float *src, int64_t batch, int64_t outer, int64_t mid,
+                         int64_t inner, int64_t s_b, int64_t s_o, int64_t s_m, int64_t s_i,
+                         int64_t *seg_off, int64_t *total_nodes, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    FSCNN_REQUIRE(total_nodes != nullptr, "total_nodes is NULL");
+    int64_t n_seg = batch * outer * mid;
+    FSCNN_REQUIRE(n_seg == 0 || (src != nullptr || inner == 0) && seg_off != nullptr, "null buffer");
+    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i};
+    return encode_offsets_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, total_nodes,
+                               workspace, workspace_bytes, as_stream(stream));
+}
+
+int fscnn_encode_nodes(const float *src, int64_t batch, int64_t outer, int64_t mid,
+                       int64_t inner, int64_t s_b, int64_t s_o, int64_t s_m, int64_t s_i,
+                       const int64_t *seg_off, fscnn_node *nodes, int64_t *matrix_off,
+                       int64_t *tensor_off, void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    int64_t n_seg = batch * outer * mid;
+    if (n_seg == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(seg_off != nullptr && nodes != nullptr, "null buffer");
+    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i};
+    cudaStream_t st = as_stream(stream);
+    int rc = encode_nodes_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, nodes, st);
+    if (rc != FSCNN_OK) return rc;
+    if (matrix_off || tensor_off) {
+        side_tables_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(
+            seg_off, n_seg, mid, outer * mid, matrix_off, tensor_off);
+        FSCNN_LAUNCH_CHECK("side_tables_kernel");
+    }
+    return FSCNN_OK;
+}
+
+int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch, int64_t outer,
+                 int64_t mid, int64_t inner, float *dst, int64_t d_b, int64_t d_o, int64_t d_m,
+                 int64_t d_i, void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    int64_t n_seg = batch * outer * mid;
+    if (n_seg == 0 || inner == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(nodes && seg_off && dst, "null buffer");
+    decode_kernel<<<(unsigned)ceil_div(n_seg, 128), 128, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2 *>(nodes), seg_off, n_seg, outer, mid, inner, dst, d_b, d_o,
+        d_m, d_i);
+    FSCNN_LAUNCH_CHECK("decode_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_sf_pack_kt(void) { return kSfPackKt; }
+
+int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int64_t *seg_off,
+                          int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+    FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && total_nodes, "bad pack arguments");
+    int64_t groups = ceil_div(k, kSfPackKt);
+    SfPackSrc src{w_kc33, k, c, kSfPackKt, kSfPackKt * 9};
+    return encode_offsets_impl(src, groups * c, false, seg_off, total_nodes, workspace,
+                               workspace_bytes, as_stream(stream));
+}
+
+int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, const int64_t *seg_off,
+                        fscnn_node *nodes, void *stream) {
+    FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && nodes, "bad pack arguments");
+    int64_t groups = ceil_div(k, kSfPackKt);
+    SfPackSrc src{w_kc33, k, c, kSfPackKt, kSfPackKt * 9};
+    return encode_nodes_impl(src, groups * c, false, seg_off, nodes, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,487 @@
+// Sparse-Filter convolution kernels.
+//
+// 1) sf_exact_kernel -- reference accumulation order, bit-exact with
+//    _conv_all_filters_kernel (layers.py:170-180) / _window_acc (kernels.py:78-97):
+//    one thread per output pixel, warp-uniform filter k; taps kw outer, kh inner,
+//    nodes ascending c; __fmul_rn + __fadd_rn (no contraction, like numba).
+//    Any geometry.  Reads the reference's CHW node buffer directly.
+//
+// 2) sf3x3_kernel -- the fast path for 3x3/s1/p1 (all VGG16 convs).  GEMM-like
+//    "dense activations x unstructured-sparse filters" on FP32 CUDA cores:
+//      * a CTA owns LI rectangular sub-regions of (4*LY) x 16 output pixels (LY*LI = 8)
+//        and 64 output channels; warp w owns filter group g (8 filters);
+//      * lane = one 4x4 output tile; it keeps acc[8 filters][4][4] in registers;
+//      * input channels stream through shared memory in chunks of CC channels: one
+//        TMA box per sub-region per chunk ((4LY+2) x 20 floats x CC, zero fill for
+//        the conv padding) plus a bulk copy of each warp's packed nonzero list for
+//        those channels, completed on an mbarrier (S-stage ring, dedicated producer
+//        warp, per-stage empty barriers so warps drift instead of lock-stepping);
+//      * per channel a lane loads its 6x6 input patch into registers (12 x LDS.128,
+//        conflict-free with the 20-float row pitch), then walks the warp-uniform
+//        nonzero list (kl, tap, value); a switch dispatches each nonzero to 16
+//        statically indexed FFMAs -- every loaded input value is reused by all
+//        nonzeros of that channel (~0.9 * 8 of them at 90% sparsity);
+//      * epilogue: + bias, optional ReLU, optional fused 2x2 max-pool (the
+//        reference's relu -> pool order, -inf start, '>' compare), float4 stores.
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace fscnn {
+namespace {
+
+// ------------------------------------------------------------------------------
+// exact, reference-order kernel
+// ------------------------------------------------------------------------------
+__global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, int w_i,
+                                const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off,
+                                int k_n, int h_f, int w_f, int stride, int pad, int n_h, int n_w,
+                                const float *__restrict__ bias, int relu, float *__restrict__ y) {
+    int k = blockIdx.y;
+    int img = blockIdx.z;
+    int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= n_h * n_w) return;
+    int i = pix / n_w, j = pix % n_w;
+    const float *xi = x + (int64_t)img * c_n * h_i * w_i;
+    int64_t seg_base = (int64_t)k * h_f * w_f;
+    float acc = 0.0f;
+    for (int l = 0; l < w_f; ++l) {
+        int w_in = l + j * stride - pad;
+        if (w_in < 0 || w_in >= w_i) continue;
+        for (int kk = 0; kk < h_f; ++kk) {
+            int h_in = kk + i * stride - pad;
+            if (h_in < 0 || h_in >= h_i) continue;
+            const float *px = xi + (int64_t)h_in * w_i + w_in;
+            int64_t p = seg_off[seg_base + (int64_t)l * h_f + kk];
+            for (int2 nd = nodes[p]; nd.x != -1; nd = nodes[++p])
+                acc = __fadd_rn(acc, __fmul_rn(px[(int64_t)nd.x * h_i * w_i], __int_as_float(nd.y)));
+        }
+    }
+    float b = bias ? bias[k] : 0.0f;
+    float v = __fadd_rn(acc, b);
+    if (relu) v = relu_np(v);
+    y[(((int64_t)img * k_n + k) * n_h + i) * n_w + j] = v;
+}
+
+// ------------------------------------------------------------------------------
+// fast 3x3 kernel
+// ------------------------------------------------------------------------------
+constexpr int KT = 4 * 2;          // filters per warp group (must match fscnn_sf_pack_kt)
+constexpr int NWARP = 8;           // consumer warps per CTA -> 64 filters per CTA
+constexpr int NTHREADS = NWARP * 32;         // warp 0 lane 0 doubles as the TMA producer
+constexpr int STAGES = 3;
+constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
+constexpr int TILE = 4;            // lane tile is TILE x TILE outputs
+constexpr int SUBW = 16;           // sub-region width (4 lanes x 4 columns)
+
+static_assert(KT == 8, "switch below is written for 8 filters per group");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+#include "sf3x3_dispatch.inc"
+
+struct Sf3Params {
+    const int2 *packed;       // packed filter stream (+16 B slack at the end)
+    const int64_t *seg_off;   // [groups][C] segment offsets
+    int64_t total_nodes;      // length of packed
+    int n, c, h, w;           // input extents (NCHW, row pitch = TMA stride)
+    int k;                    // output channels
+    int ldo;                  // output row pitch (floats)
+    int tiles_h, tiles_w;     // sub-region grid per image
+    int n_sub;                // n * tiles_h * tiles_w
+    int cc;                   // channels per chunk
+    int ent_cap;              // entry slots per warp per stage (int2)
+    int box_floats;           // floats per sub-region box per stage
+    const float *bias;
+    float *y;
+    int relu;
+    int pool;                 // fused 2x2 max-pool
+    int dbg;                  // debug: 1 = walk entries without FMAs, 3 = no TMA, 4 = no bulk copies
+};
+
+template <int LY>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
+    constexpr int LI = 8 / LY;          // sub-regions per CTA
+    constexpr int SUBH = TILE * LY;     // sub-region height
+    constexpr int BOXH = SUBH + 2;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float *in_s = reinterpret_cast<float *>(smem_raw);
+    const int stage_in_floats = LI * p.box_floats;
+    int2 *ent_s = reinterpret_cast<int2 *>(in_s + STAGES * stage_in_floats);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ent_s + STAGES * NWARP * p.ent_cap);
+    uint64_t *empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub0 = blockIdx.x * LI;
+    const int g0 = blockIdx.y * NWARP;
+    const int n_groups = (p.k + KT - 1) / KT;
+    const int n_chunks = (p.c + p.cc - 1) / p.cc;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWARP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    __syncthreads();
+
+    // Producer: fill one stage with chunk `ch` (TMA boxes + the 8 warps' entry runs).
+    auto produce = [&](int ch) {
+        const int s = ch % STAGES;
+        const int c0 = ch * p.cc;
+        const int cnt = min(p.cc, p.c - c0);
+        uint32_t bytes = 0;
+        int64_t lo[NWARP], len16[NWARP];
+#pragma unroll
+        for (int wv = 0; wv < NWARP; ++wv) {
+            int g = g0 + wv;
+            lo[wv] = 0;
+            len16[wv] = 0;
+            if (g < n_groups) {
+                int64_t a = p.seg_off[(int64_t)g * p.c + c0];
+                int64_t sidx = (int64_t)g * p.c + c0 + cnt;
+                int64_t b = (sidx < (int64_t)n_groups * p.c) ? p.seg_off[sidx] : p.total_nodes;
+                int64_t a2 = a & ~int64_t(1);  // 16-byte aligned start
+                int64_t nb = ((b - a2) * 8 + 15) & ~int64_t(15);
+                lo[wv] = a2;
+                len16[wv] = nb;
+                if (p.dbg != 4) bytes += (uint32_t)nb;
+            }
+        }
+        int n_box = 0;
+#pragma unroll
+        for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
+        // a box always moves cc channels (OOB ones zero-filled) and counts them all
+        if (p.dbg != 3) bytes += (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
+        mbar_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int wv = 0; wv < NWARP; ++wv)
+            if (len16[wv] > 0 && p.dbg != 4)
+                bulk_load(ent_s + (s * NWARP + wv) * p.ent_cap, p.packed + lo[wv],
+                          (uint32_t)len16[wv], &full[s]);
+#pragma unroll
+        for (int li = 0; li < LI; ++li) {
+            int sub = sub0 + li;
+            if (sub >= p.n_sub || p.dbg == 3) continue;
+            int tw = sub % p.tiles_w;
+            int r = sub / p.tiles_w;
+            int th = r % p.tiles_h;
+            int img = r / p.tiles_h;
+            // box covers rows th*SUBH-1 .. +SUBH and logical cols tw*SUBW-1 .. +18, i.e.
+            // memory cols tw*SUBW .. +19 of the halo-column layout (16-byte aligned start:
+            // the TMA unit faults on a misaligned innermost coordinate)
+            tma_load_4d(in_s + s * stage_in_floats + li * p.box_floats, &tmap, &full[s],
+                        tw * SUBW, th * SUBH - 1, c0, img);
+        }
+    };
+    const bool producer = (threadIdx.x == 0);
+    if (producer)
+        for (int ch = 0; ch < STAGES && ch < n_chunks; ++ch) produce(ch);
+    __syncwarp();  // the dispatch loop's .uni branches need a converged warp
+
+    const int lx = lane & 3;
+    const int ly = (lane >> 2) % LY;
+    const int li = lane / (4 * LY);
+    const int g = g0 + warp;
+
+    float acc[KT][TILE][TILE];
+#pragma unroll
+    for (int a = 0; a < KT; ++a)
+#pragma unroll
+        for (int b = 0; b < TILE; ++b)
+#pragma unroll
+            for (int d = 0; d < TILE; ++d) acc[a][b][d] = 0.0f;
+
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int s = ch % STAGES;
+        mbar_wait(&full[s], (ch / STAGES) & 1);
+        __syncwarp();
+        const int c0 = ch * p.cc;
+        const int cnt = min(p.cc, p.c - c0);
+        if (g < n_groups) {
+            const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
+            const int e0 = (int)(p.seg_off[(int64_t)g * p.c + c0] & 1);  // offset inside aligned copy
+            uint32_t cur = smem_u32(ents + e0);
+            const float *box = in_s + s * stage_in_floats + li * p.box_floats;
+            for (int cc = 0; cc < cnt; ++cc) {
+                const float *rowp = box + (cc * BOXH + TILE * ly) * BOXW + TILE * lx;
+                float pt[6][6];
+#pragma unroll
+                for (int r = 0; r < 6; ++r) {
+                    float4 a = *reinterpret_cast<const float4 *>(rowp + r * BOXW);
+                    float2 b = *reinterpret_cast<const float2 *>(rowp + r * BOXW + 4);
+                    pt[r][0] = a.x; pt[r][1] = a.y; pt[r][2] = a.z; pt[r][3] = a.w;
+                    pt[r][4] = b.x; pt[r][5] = b.y;
+                }
+                if (p.dbg >= 3) {
+                    // garbage entries: do not walk them
+                } else if (p.dbg == 0) {
+                    cur = sf3x3_channel(acc, pt, cur);
+                } else {
+                    const int2 *ep = reinterpret_cast<const int2 *>(ents) + ((cur - smem_u32(ents)) >> 3);
+                    for (;;) {
+                        const int2 en = *ep++;
+                        if (en.x < 0) break;
+                    }
+                    cur = smem_u32(ep);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // Refill the stage consumed one chunk ago (prefetch distance STAGES-1), once
+        // every warp has released it; by then it is usually already free.
+        if (producer && ch >= 1) {
+            const int prev = ch - 1;
+            const int nxt = prev + STAGES;
+            if (nxt < n_chunks) {
+                mbar_wait(&empty[prev % STAGES], (prev / STAGES) & 1);
+                produce(nxt);
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---------------- epilogue ----------------
+    const int sub = sub0 + li;
+    if (g >= n_groups || sub >= p.n_sub) return;
+    const int tw = sub % p.tiles_w;
+    const int r = sub / p.tiles_w;
+    const int th = r % p.tiles_h;
+    const int img = r / p.tiles_h;
+    const int y0 = th * SUBH + TILE * ly;
+    const int x0 = tw * SUBW + TILE * lx;
+    if (y0 >= p.h || x0 >= p.w) return;
+#pragma unroll
+    for (int kl = 0; kl < KT; ++kl) {
+        const int k = g * KT + kl;
+        if (k >= p.k) break;
+        const float b = p.bias ? p.bias[k] : 0.0f;
+        float o[TILE][TILE];
+#pragma unroll
+        for (int py = 0; py < TILE; ++py)
+#pragma unroll
+            for (int px = 0; px < TILE; ++px) {
+                float v = acc[kl][py][px] + b;
+                o[py][px] = p.relu ? relu_np(v) : v;
+            }
+        if (!p.pool) {
+            // halo-column layout: logical column x lives at memory column x + 1
+            float *dst = p.y + (((int64_t)img * p.k + k) * p.h + y0) * p.ldo + x0 + 1;
+#pragma unroll
+            for (int py = 0; py < TILE; ++py) {
+                if (y0 + py >= p.h) break;
+#pragma unroll
+                for (int px = 0; px < TILE; ++px)
+                    if (x0 + px < p.w) dst[(int64_t)py * p.ldo + px] = o[py][px];
+            }
+        } else {
+            // fused 2x2/2 max-pool: output (h/2, w/2) with row pitch ldo
+            const int ho = p.h >> 1, wo = p.w >> 1;
+            const int yo0 = y0 >> 1, xo0 = x0 >> 1;
+            float *dst = p.y + (((int64_t)img * p.k + k) * ho + yo0) * p.ldo + xo0 + 1;
+#pragma unroll
+            for (int qy = 0; qy < 2; ++qy) {
+                if (yo0 + qy >= ho) break;
+#pragma unroll
+                for (int qx = 0; qx < 2; ++qx) {
+                    if (xo0 + qx >= wo) break;
+                    float m = -INFINITY;
+#pragma unroll
+                    for (int ph = 0; ph < 2; ++ph)
+#pragma unroll
+                        for (int pw = 0; pw < 2; ++pw) {
+                            float v = o[2 * qy + ph][2 * qx + pw];
+                            if (v > m) m = v;
+                        }
+                    dst[(int64_t)qy * p.ldo + qx] = m;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+template <int LY>
+int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
+    constexpr int LI = 8 / LY;
+    constexpr int SUBH = TILE * LY;
+    p.tiles_h = (int)ceil_div(p.h, SUBH);
+    p.tiles_w = (int)ceil_div(p.w, SUBW);
+    p.n_sub = p.n * p.tiles_h * p.tiles_w;
+    p.box_floats = BOXW * (SUBH + 2) * p.cc;
+    // each box must start 128-byte aligned (TMA destination)
+    p.box_floats = (p.box_floats + 31) & ~31;
+    size_t smem = (size_t)STAGES * LI * p.box_floats * 4 + (size_t)STAGES * NWARP * p.ent_cap * 8 +
+                  2 * STAGES * 8;
+    if (smem > 227 * 1024) {
+        set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
+        return FSCNN_ERR_UNSUPPORTED;
+    }
+    auto kern = sf3x3_kernel<LY>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        set_error("sf3x3: smem attribute (%zu bytes): %s", smem, cudaGetErrorString(e));
+        return FSCNN_ERR_CUDA;
+    }
+    int n_groups = (int)ceil_div(p.k, KT);
+    dim3 grid((unsigned)ceil_div(p.n_sub, LI), (unsigned)ceil_div(n_groups, NWARP));
+    kern<<<grid, NTHREADS, smem, st>>>(map, p);
+    return check_launch("sf3x3_kernel");
+}
+
+}  // namespace
+}  // namespace fscnn
+
+using namespace fscnn;
+
+extern "C" {
+
+int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_node *nodes,
+                        const int64_t *seg_off, int k, int h_f, int w_f, int stride, int pad,
+                        const float *bias, int relu, float *y, void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
+    FSCNN_REQUIRE(h_f > 0 && w_f > 0 && stride > 0 && pad >= 0, "bad geometry");
+    FSCNN_REQUIRE(h_f <= h + 2 * pad && w_f <= w + 2 * pad, "filter exceeds padded input");
+    int n_h = (h + 2 * pad - h_f) / stride + 1;
+    int n_w = (w + 2 * pad - w_f) / stride + 1;
+    if (n == 0 || k == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && nodes && seg_off && y, "null buffer");
+    FSCNN_REQUIRE(k <= 65535 && n <= 65535, "k or n too large for the grid");
+    dim3 grid((unsigned)ceil_div((int64_t)n_h * n_w, 128), (unsigned)k, (unsigned)n);
+    sf_exact_kernel<<<grid, 128, 0, as_stream(stream)>>>(
+        x, c, h, w, reinterpret_cast<const int2 *>(nodes), seg_off, k, h_f, w_f, stride, pad, n_h,
+        n_w, bias, relu, y);
+    FSCNN_LAUNCH_CHECK("sf_exact_kernel");
+    return FSCNN_OK;
+}
+
+// Extended entry: ldi/ldo are input/output row pitches (floats, multiples of 4);
+// pool fuses the 2x2 max-pool; cc/ent_cap/ly are tuning knobs (0 = auto).
+int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
+                        const fscnn_node *packed, const int64_t *packed_seg_off,
+                        int64_t total_nodes, int max_chunk_entries, int cc, int k,
+                        const float *bias, int relu, int pool, float *y, int ldo, int ly,
+                        void *stream) {
+    static const int dbg_mode = getenv("FSCNN_SF3_DEBUG") ? atoi(getenv("FSCNN_SF3_DEBUG")) : 0;
+    FSCNN_REQUIRE(n > 0 && c > 0 && h > 0 && w > 0 && k > 0, "bad extents");
+    FSCNN_REQUIRE(ldi >= w + 1 && ldi % 4 == 0, "input row pitch must be >= w + 1 and a multiple of 4");
+    FSCNN_REQUIRE(ldo >= (pool ? w / 2 : w) + 1, "output row pitch too small");
+    FSCNN_REQUIRE(x && packed && packed_seg_off && y, "null buffer");
+    FSCNN_REQUIRE(cc > 0 && cc <= 256, "bad channel chunk");
+    FSCNN_REQUIRE(max_chunk_entries > 0, "bad entry capacity");
+    FSCNN_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, "input must be 16-byte aligned");
+    if (pool) FSCNN_REQUIRE(h % 2 == 0 && w % 2 == 0, "fused pool needs even extents");
+    EncodeTiledFn enc = get_encode_tiled();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return FSCNN_ERR_CUDA;
+    }
+    Sf3Params p{};
+    p.packed = reinterpret_cast<const int2 *>(packed);
+    p.seg_off = packed_seg_off;
+    p.total_nodes = total_nodes;
+    p.n = n; p.c = c; p.h = h; p.w = w; p.k = k;
+    p.ldo = ldo;
+    p.cc = cc;
+    // aligned-down start can add one entry, round-up to 16 B another
+    p.ent_cap = (max_chunk_entries + 3 + 1) & ~1;
+    p.bias = bias; p.y = y; p.relu = relu; p.pool = pool;
+    p.dbg = dbg_mode;
+    if (ly <= 0) ly = (h >= 128) ? 8 : (h >= 64 ? 4 : 2);
+    int sub_h = TILE * ly;
+    CUtensorMap map;
+    cuuint64_t gdim[4] = {(cuuint64_t)w + 1, (cuuint64_t)h, (cuuint64_t)c, (cuuint64_t)n};
+    cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * h * 4,
+                             (cuuint64_t)ldi * h * c * 4};
+    cuuint32_t box[4] = {(cuuint32_t)BOXW, (cuuint32_t)(sub_h + 2), (cuuint32_t)cc, 1};
+    cuuint32_t estride[4] = {1, 1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride,
+                     box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return FSCNN_ERR_CUDA;
+    }
+    cudaStream_t st = as_stream(stream);
+    switch (ly) {
+        case 8: return launch_sf3x3<8>(map, p, st);
+        case 4: return launch_sf3x3<4>(map, p, st);
+        case 2: return launch_sf3x3<2>(map, p, st);
+        default: set_error("unsupported sub-region height %d", ly); return FSCNN_ERR_ARG;
+    }
+}
+
+}  // extern "C"

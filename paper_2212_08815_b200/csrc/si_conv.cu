@@ -1,0 +1,80 @@
+// Sparse-Input convolution, bit-exact with _conv_input_sparse_kernel
+// (kernels.py:136-166) for all K filters of a layer at once.
+//
+// Gather form over the reference's CHW node format: output (n, k, i, j) walks
+// taps kw outer, kh inner, and the input channel fiber at (w_in, h_in) in ascending
+// c, accumulating filt[k][c][kh][kw] * v with separate fp32 multiply and add.
+// Mapping: a warp owns one output pixel and 32 consecutive filters (lane = k), so
+// the node stream is warp-uniform (broadcast loads) and the weight loads from the
+// transposed [c][kh][kw][K] bank are one coalesced 128-byte line per node.
+// Results equal to zero are written as +0.0 (the reference stores no node and
+// densify yields +0.0), then + bias[k] when a bias is given (layers.py:425-428).
+#include "common.cuh"
+
+namespace fscnn {
+namespace {
+
+constexpr int kPixPerBlock = 8;  // warps per block, one output pixel each
+
+__global__ void __launch_bounds__(kPixPerBlock * 32)
+    si_gather_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int c_n,
+                     int h_i, int w_i, const float *__restrict__ wt, int k_n, int h_f, int w_f,
+                     int stride, int pad, int n_h, int n_w, const float *__restrict__ bias,
+                     float *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int pix = blockIdx.x * kPixPerBlock + (threadIdx.x >> 5);
+    const int k = blockIdx.y * 32 + lane;
+    const int img = blockIdx.z;
+    if (pix >= n_h * n_w) return;
+    const int i = pix / n_w, j = pix % n_w;
+    const int64_t *so = seg_off + (int64_t)img * h_i * w_i;
+    const bool live = k < k_n;
+    float acc = 0.0f;
+    for (int l = 0; l < w_f; ++l) {
+        int w_in = l + j * stride - pad;
+        if (w_in < 0 || w_in >= w_i) continue;
+        for (int kk = 0; kk < h_f; ++kk) {
+            int h_in = kk + i * stride - pad;
+            if (h_in < 0 || h_in >= h_i) continue;
+            int64_t q = so[(int64_t)w_in * h_i + h_in];
+            const float *wrow = wt + ((int64_t)kk * w_f + l) * k_n + (live ? k : 0);
+            const int64_t cstride = (int64_t)h_f * w_f * k_n;
+            for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) {
+                float wv = wrow[(int64_t)nd.x * cstride];
+                acc = __fadd_rn(acc, __fmul_rn(wv, __int_as_float(nd.y)));
+            }
+        }
+    }
+    if (!live) return;
+    float v = (acc != 0.0f) ? acc : 0.0f;
+    if (bias) v = __fadd_rn(v, bias[k]);
+    y[(((int64_t)img * k_n + k) * n_h + i) * n_w + j] = v;
+}
+
+}  // namespace
+}  // namespace fscnn
+
+using namespace fscnn;
+
+extern "C" {
+
+int fscnn_si_conv(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
+                  int w, const float *wt, int k, int h_f, int w_f, int stride, int pad,
+                  const float *bias, float *y, void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
+    FSCNN_REQUIRE(h_f > 0 && w_f > 0 && stride > 0 && pad >= 0, "bad geometry");
+    FSCNN_REQUIRE(h_f <= h + 2 * pad && w_f <= w + 2 * pad, "filter exceeds padded input");
+    if (n == 0 || k == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(in_nodes && in_seg_off && wt && y, "null buffer");
+    int n_h = (h + 2 * pad - h_f) / stride + 1;
+    int n_w = (w + 2 * pad - w_f) / stride + 1;
+    dim3 grid((unsigned)ceil_div((int64_t)n_h * n_w, kPixPerBlock), (unsigned)ceil_div(k, 32),
+              (unsigned)n);
+    si_gather_kernel<<<grid, kPixPerBlock * 32, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2 *>(in_nodes), in_seg_off, c, h, w, wt, k, h_f, w_f, stride,
+        pad, n_h, n_w, bias, y);
+    FSCNN_LAUNCH_CHECK("si_gather_kernel");
+    return FSCNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,343 @@
+"""Device-side operators: thin typed wrappers over the C ABI on torch CUDA tensors.
+
+Everything here is stream-ordered on torch's current stream and allocates its outputs
+with torch (the caching allocator).  The only host synchronisations are the ones the
+node format forces: an encoder must learn its node count before it can size the node
+buffer (count -> scan -> read total -> write), exactly the reference's two-pass
+_build_segmented (sparse_core.py:319-331).
+
+Tensor conventions
+  dense activations   torch.float32 [N, C, H, W] (row pitch may exceed W, see ldw)
+  node buffers        torch.int32 [n_nodes, 2]  -- byte-identical to NODE_DTYPE
+  offset tables       torch.int64
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream
+
+NODE_DTYPE = np.dtype([("index", "<i4"), ("value", "<f4")])
+
+
+def _dev():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def nodes_to_numpy(nodes: torch.Tensor, count: int | None = None) -> np.ndarray:
+    """Device node buffer -> reference NODE_DTYPE array (bit copy)."""
+    t = nodes if count is None else nodes[:count]
+    return t.cpu().numpy().view(NODE_DTYPE).reshape(-1)
+
+
+def nodes_from_numpy(nodes: np.ndarray, slack: int = 0) -> torch.Tensor:
+    """Reference NODE_DTYPE array -> device int32 [n + slack, 2] (bit copy)."""
+    a = np.ascontiguousarray(nodes).view(np.int32).reshape(-1, 2)
+    out = torch.empty((a.shape[0] + slack, 2), dtype=torch.int32, device=_dev())
+    if a.shape[0]:
+        out[: a.shape[0]].copy_(torch.from_numpy(a), non_blocking=False)
+    if slack:
+        out[a.shape[0]:].fill_(-1)
+    return out
+
+
+# -- encoder / decoder ---------------------------------------------------------------
+
+
+@dataclass
+class Encoded:
+    """Output of the device encoder for a batch of arranged tensors."""
+
+    nodes: torch.Tensor          # int32 [n_nodes (+slack), 2]
+    n_nodes: int
+    seg_off: torch.Tensor        # int64 [batch*outer*mid]
+    matrix_off: torch.Tensor     # int64 [batch*outer]
+    tensor_off: torch.Tensor     # int64 [batch]
+
+
+def encode(src: torch.Tensor, batch: int, outer: int, mid: int, inner: int,
+           strides: tuple[int, int, int, int], slack: int = 0) -> Encoded:
+    """Node-format encoding of ``batch`` arranged (outer, mid, inner) views of ``src``.
+
+    strides = (s_b, s_o, s_m, s_i) in elements.  Restates sparsify_tensor3 /
+    SparseTensor4.stack (sparse_core.py:273-353) on the device; see fscnn_encode_*.
+    """
+    dev = _dev()
+    s_b, s_o, s_m, s_i = (int(v) for v in strides)
+    n_seg = batch * outer * mid
+    seg = torch.empty(max(n_seg, 1), dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)
+    ws_bytes = int(_lib.load().fscnn_encode_workspace_bytes(n_seg))
+    ws = torch.empty(ws_bytes // 8 + 1, dtype=torch.int64, device=dev)
+    st = stream()
+    call("fscnn_encode_offsets", ptr(src), batch, outer, mid, inner, s_b, s_o, s_m, s_i,
+         ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
+    n_nodes = int(total.item())  # the format's one forced sync: size the node buffer
+    nodes = torch.empty((n_nodes + slack, 2), dtype=torch.int32, device=dev)
+    if slack:
+        nodes[n_nodes:].fill_(-1)
+    mat = torch.empty(max(batch * outer, 1), dtype=torch.int64, device=dev)
+    ten = torch.empty(max(batch, 1), dtype=torch.int64, device=dev)
+    call("fscnn_encode_nodes", ptr(src), batch, outer, mid, inner, s_b, s_o, s_m, s_i,
+         ptr(seg), ptr(nodes), ptr(mat), ptr(ten), st)
+    return Encoded(nodes, n_nodes, seg[:n_seg], mat[: batch * outer], ten[:batch])
+
+
+# (inner, mid, outer) axis ids 0=C 1=H 2=W per order name (sparse_core.py:44-66)
+ORDER_AXES = {
+    "WHC": (2, 1, 0),
+    "WCH": (2, 0, 1),
+    "HWC": (1, 2, 0),
+    "HCW": (1, 0, 2),
+    "CHW": (0, 1, 2),
+    "CWH": (0, 2, 1),
+}
+
+
+def encode_order(x: torch.Tensor, order: str, slack: int = 0) -> Encoded:
+    """Encode a [B, C, H, W]-indexed tensor (any strides) in the named axis order."""
+    assert x.dim() == 4
+    inner_ax, mid_ax, outer_ax = ORDER_AXES[order]
+    dims = x.shape[1:]
+    st = x.stride()
+    es = (st[1], st[2], st[3])  # element strides of c, h, w
+    return encode(x, x.shape[0], dims[outer_ax], dims[mid_ax], dims[inner_ax],
+                  (st[0], es[outer_ax], es[mid_ax], es[inner_ax]), slack)
+
+
+def decode(nodes: torch.Tensor, seg_off: torch.Tensor, batch: int, outer: int, mid: int,
+           inner: int, out: torch.Tensor, strides: tuple[int, int, int, int]) -> torch.Tensor:
+    """Write every element of the strided destination view from node format."""
+    d_b, d_o, d_m, d_i = (int(v) for v in strides)
+    call("fscnn_decode", ptr(nodes), ptr(seg_off), batch, outer, mid, inner, ptr(out),
+         d_b, d_o, d_m, d_i, stream())
+    return out
+
+
+def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None = None):
+    """Inverse of encode_order: returns a dense [B, C, H, W] tensor."""
+    b = dims_bchw[0]
+    dims = dims_bchw[1:]
+    if out is None:
+        out = torch.empty(tuple(dims_bchw), dtype=torch.float32, device=_dev())
+    inner_ax, mid_ax, outer_ax = ORDER_AXES[order]
+    st = out.stride()
+    es = (st[1], st[2], st[3])
+    return decode(nodes, seg_off, b, dims[outer_ax], dims[mid_ax], dims[inner_ax], out,
+                  (st[0], es[outer_ax], es[mid_ax], es[inner_ax]))
+
+
+# -- sparse-filter conv ------------------------------------------------------------------
+
+STAGES, NWARP, BOXW, SUBW, TILE = 3, 8, 20, 16, 4
+SMEM_LIMIT = 227 * 1024
+
+
+def _align(v: int, a: int) -> int:
+    return (v + a - 1) // a * a
+
+
+def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int) -> int:
+    li = 8 // ly
+    box = _align(BOXW * (TILE * ly + 2) * cc, 32)
+    return STAGES * li * box * 4 + STAGES * NWARP * ent_cap * 8 + 2 * STAGES * 8
+
+
+def pick_ly(h: int) -> int:
+    """Sub-region height 4*ly with the least padded rows (ties -> taller regions)."""
+    best = None
+    for ly in (8, 4, 2):
+        rows = math.ceil(h / (TILE * ly)) * TILE * ly
+        key = (rows, -ly)
+        if best is None or key < best[0]:
+            best = (key, ly)
+    return best[1]
+
+
+@dataclass
+class PackedBank:
+    """A filter bank in the fast kernel's channel-major packed stream (device)."""
+
+    k: int
+    c: int
+    nodes: torch.Tensor        # int32 [total + 2, 2]
+    seg_off: torch.Tensor      # int64 [groups * c]
+    total: int
+    counts: np.ndarray         # host: nodes per (group, channel) incl. sentinel
+    nnz: int                   # nonzero weights
+    _cache: dict = None
+
+    def chunk_plan(self, ly: int) -> tuple[int, int]:
+        """(cc, max_chunk_entries) fitting shared memory for sub-region height ly."""
+        if self._cache is None:
+            self._cache = {}
+        if ly in self._cache:
+            return self._cache[ly]
+        for cc in (8, 4, 2, 1):
+            if cc > self.c and cc != 1:
+                continue
+            n_chunks = math.ceil(self.c / cc)
+            pad = n_chunks * cc - self.c
+            cnt = np.pad(self.counts, ((0, 0), (0, pad)))
+            mx = int(cnt.reshape(cnt.shape[0], n_chunks, cc).sum(axis=2).max())
+            ent_cap = (mx + 4) & ~1
+            if sf3x3_smem_bytes(ly, cc, ent_cap) <= SMEM_LIMIT:
+                self._cache[ly] = (cc, mx)
+                return cc, mx
+        raise RuntimeError("filter bank too dense for the fast kernel's shared memory")
+
+
+def sf_pack(w_kc33: torch.Tensor) -> PackedBank:
+    """Pack a dense [K, C, 3, 3] bank (device) into the fast kernel's stream."""
+    assert w_kc33.dim() == 4 and tuple(w_kc33.shape[2:]) == (3, 3)
+    w = w_kc33.contiguous()
+    k, c = int(w.shape[0]), int(w.shape[1])
+    kt = int(_lib.load().fscnn_sf_pack_kt())
+    groups = math.ceil(k / kt)
+    dev = _dev()
+    seg = torch.empty(groups * c, dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)
+    ws_bytes = int(_lib.load().fscnn_encode_workspace_bytes(groups * c))
+    ws = torch.empty(ws_bytes // 8 + 1, dtype=torch.int64, device=dev)
+    st = stream()
+    call("fscnn_sf_pack_offsets", ptr(w), k, c, ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
+    n = int(total.item())
+    nodes = torch.empty((n + 2, 2), dtype=torch.int32, device=dev)
+    nodes[n:].fill_(-1)
+    call("fscnn_sf_pack_nodes", ptr(w), k, c, ptr(seg), ptr(nodes), st)
+    so = seg.cpu().numpy()
+    ends = np.append(so[1:], n)
+    counts = (ends - so).reshape(groups, c)
+    return PackedBank(k, c, nodes, seg, n, counts, int(n - groups * c))
+
+
+def halo_pitch(w: int) -> int:
+    """Row pitch of the halo-column layout: logical column j at memory column j+1,
+    column 0 and columns > w zero, pitch a multiple of 4 floats (16 B, TMA stride)."""
+    return _align(w + 1, 4)
+
+
+def halo_empty(n: int, c: int, h: int, w: int, device=None) -> torch.Tensor:
+    """Zeroed [N, C, H, halo_pitch(w)] buffer (the kernels never write the halo columns)."""
+    return torch.zeros((n, c, h, halo_pitch(w)), dtype=torch.float32, device=device or _dev())
+
+
+def to_halo(x: torch.Tensor) -> torch.Tensor:
+    """Dense [N, C, H, W] -> halo-column layout copy."""
+    n, c, h, w = (int(v) for v in x.shape)
+    out = halo_empty(n, c, h, w, x.device)
+    out[..., 1 : w + 1] = x
+    return out
+
+
+def from_halo(xh: torch.Tensor, w: int) -> torch.Tensor:
+    """View of the logical [N, C, H, W] data inside a halo-column buffer."""
+    return xh[..., 1 : w + 1]
+
+
+def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, relu: bool,
+               pool: bool, out: torch.Tensor | None = None, w: int | None = None,
+               ly: int = 0) -> torch.Tensor:
+    """Fast 3x3/s1/p1 sparse-filter conv (+ReLU, +fused 2x2 max-pool).
+
+    ``x`` is a halo-column buffer [N, C, H, pitch] (see halo_pitch) holding a logical
+    width ``w`` (default pitch - 1).  Returns the halo-column output buffer
+    [N, K, H', pitch'] (H' = H/2 with the fused pool); use from_halo to view it.
+    """
+    n, c, h = int(x.shape[0]), int(x.shape[1]), int(x.shape[2])
+    ldi = int(x.stride(2))
+    w = ldi - 1 if w is None else int(w)
+    assert x.stride(3) == 1 and x.stride(1) == ldi * h and x.stride(0) == ldi * h * c
+    assert c == bank.c and ldi >= w + 1
+    if ly <= 0:
+        ly = pick_ly(h)
+    cc, mx = bank.chunk_plan(ly)
+    ho, wo = (h // 2, w // 2) if pool else (h, w)
+    if out is None:
+        out = halo_empty(n, bank.k, ho, wo, x.device)
+    ldo = int(out.stride(2))
+    call("fscnn_sf_conv3x3_ex", ptr(x), n, c, h, w, ldi, ptr(bank.nodes), ptr(bank.seg_off),
+         bank.total, mx, cc, bank.k, ptr(bias), int(relu), int(pool), ptr(out), ldo, ly, stream())
+    return out
+
+
+def sf_conv_exact(x: torch.Tensor, nodes: torch.Tensor, seg_off: torch.Tensor, k: int, h_f: int,
+                  w_f: int, stride_: int, pad: int, bias: torch.Tensor | None, relu: bool = False,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Reference-order sparse-filter conv (bit-exact with layers.py:170-180)."""
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    n_h = (h + 2 * pad - h_f) // stride_ + 1
+    n_w = (w + 2 * pad - w_f) // stride_ + 1
+    if out is None:
+        out = torch.empty((n, k, n_h, n_w), dtype=torch.float32, device=x.device)
+    call("fscnn_sf_conv_exact", ptr(x), n, c, h, w, ptr(nodes), ptr(seg_off), k, h_f, w_f,
+         stride_, pad, ptr(bias), int(relu), ptr(out), stream())
+    return out
+
+
+# -- sparse-input conv --------------------------------------------------------------------
+
+
+def kcrs_to_crsk(w: torch.Tensor) -> torch.Tensor:
+    w = w.contiguous()
+    k, c, r, s = (int(v) for v in w.shape)
+    out = torch.empty((c, r, s, k), dtype=torch.float32, device=w.device)
+    call("fscnn_kcrs_to_crsk", ptr(w), k, c, r, s, ptr(out), stream())
+    return out
+
+
+def si_conv(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,
+            wt_crsk: torch.Tensor, k: int, h_f: int, w_f: int, stride_: int, pad: int,
+            bias: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Sparse-input conv over CHW node tensors (bit-exact with kernels.py:136-166)."""
+    n_h = (h + 2 * pad - h_f) // stride_ + 1
+    n_w = (w + 2 * pad - w_f) // stride_ + 1
+    if out is None:
+        out = torch.empty((n, k, n_h, n_w), dtype=torch.float32, device=nodes.device)
+    call("fscnn_si_conv", ptr(nodes), ptr(seg_off), n, c, h, w, ptr(wt_crsk), k, h_f, w_f,
+         stride_, pad, ptr(bias), ptr(out), stream())
+    return out
+
+
+# -- dense layers / layout ----------------------------------------------------------------
+
+
+def relu(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    x = x.contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    call("fscnn_relu", ptr(x), x.numel(), ptr(out), stream())
+    return out
+
+
+def pool2d(x: torch.Tensor, h_p: int, w_p: int, use_max: bool, out=None) -> torch.Tensor:
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty((n, c, h // h_p, w // w_p), dtype=torch.float32, device=x.device)
+    call("fscnn_pool2d", ptr(x), n, c, h, w, h_p, w_p, int(use_max), ptr(out), stream())
+    return out
+
+
+def whc_to_nchw(x_whc: torch.Tensor, n: int, c: int, h: int, w: int, out=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty((n, c, h, w), dtype=torch.float32, device=x_whc.device)
+    call("fscnn_whc_to_nchw", ptr(x_whc), n, c, h, w, ptr(out), stream())
+    return out
+
+
+def nchw_to_whc(x: torch.Tensor, out=None) -> torch.Tensor:
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty((n, w, h, c), dtype=torch.float32, device=x.device)
+    call("fscnn_nchw_to_whc", ptr(x), n, c, h, w, ptr(out), stream())
+    return out

@@ -1,0 +1,157 @@
+"""Device-resident VGG16-shaped sparse-filter conv stack (the BASELINE config 3/5 path).
+
+Mirrors network.prepare + network.forward for the ``vgg16_desk`` stack in the
+``sparse_filter`` variant (network.py:345-407, :410-534, plan :541): 13 3x3/s1/p1
+convs, ReLU after each, 2x2 max-pool after each block.  On the device every
+conv -> ReLU [-> max-pool] group is ONE launch of the fast sparse-filter kernel
+(ReLU and pool fused into its epilogue, in the reference's relu -> pool order), and
+activations stay in HBM between layers in NCHW "halo-column" buffers (logical column j
+at memory column j+1, zero columns around it, 16-byte row pitch) so every TMA box the
+kernel loads starts 16-byte aligned.
+
+Preparation encodes each dense filter bank on the GPU into the reference's CHW
+SparseTensor4 node format (kept, bit-exact with sparsify_tensor3 + stack) and packs
+it into the kernel's channel-major stream.  Multi-GPU runs replicate the encoded
+banks (see distributed.py) and shard the batch.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device
+from .workloads import VGG16_PLAN
+
+
+@dataclass
+class ConvStep:
+    k: int
+    c: int
+    h: int
+    w: int
+    pool: bool
+    bank: device.PackedBank
+    bias: torch.Tensor
+    nodes: torch.Tensor      # reference CHW node buffer (SparseTensor4.nodes)
+    seg_off: torch.Tensor    # SparseTensor4.segment_offsets, [K*9]
+    tensor_off: torch.Tensor
+    matrix_off: torch.Tensor
+    n_nodes: int
+    ly: int = 0
+
+
+def _align4(v: int) -> int:
+    return (v + 3) // 4 * 4
+
+
+class VGGEngine:
+    """Prepared VGG16 conv stack on one GPU.
+
+    layers: list of (filters (K, C, 3, 3) float32, bias (K,)) in plan order -- numpy
+    arrays (uploaded here) or CUDA tensors; or pre-encoded banks via ``from_encoded``.
+    """
+
+    def __init__(self, layers, batch: int, hw: int = 224, plan=VGG16_PLAN, in_c: int = 3,
+                 encoded=None):
+        self.batch, self.hw, self.plan = batch, hw, list(plan)
+        self.in_c = in_c
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.steps: list[ConvStep] = []
+        c, h = in_c, hw
+        li = 0
+        conv_idx = [i for i, it in enumerate(self.plan) if it != "M"]
+        for pos in conv_idx:
+            pool = pos + 1 < len(self.plan) and self.plan[pos + 1] == "M"
+            if encoded is not None:
+                nodes, n_nodes, seg, ten, mat, bias_np, k = encoded[li]
+                dense = torch.empty((k, c, 3, 3), dtype=torch.float32, device=dev)
+                device.decode(nodes, seg, k, 3, 3, c, dense, (c * 9, 1, 3, 9))
+                bias_t = torch.as_tensor(np.asarray(bias_np, np.float32)).to(dev)
+            else:
+                filt, bias_np = layers[li]
+                dense = torch.as_tensor(np.asarray(filt, np.float32) if not torch.is_tensor(filt) else filt)
+                dense = dense.to(dev, torch.float32).contiguous()
+                k = int(dense.shape[0])
+                assert tuple(dense.shape[1:]) == (c, 3, 3), (dense.shape, c)
+                enc = device.encode_order(dense, "CHW")
+                nodes, n_nodes, seg, ten, mat = enc.nodes, enc.n_nodes, enc.seg_off, enc.tensor_off, enc.matrix_off
+                bias_t = torch.as_tensor(np.asarray(bias_np, np.float32) if not torch.is_tensor(bias_np) else bias_np)
+                bias_t = bias_t.to(dev, torch.float32).contiguous()
+            bank = device.sf_pack(dense)
+            self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes,
+                                       device.pick_ly(h)))
+            c = k
+            if pool:
+                h //= 2
+            li += 1
+        self.out_c, self.out_hw = c, h
+        self._bufs = None
+        self._bufs_batch = None
+
+    # -- buffers ------------------------------------------------------------------------
+    def _buffers(self, n: int):
+        if self._bufs is None or self._bufs_batch != n:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self._in = device.halo_empty(n, self.in_c, self.hw, self.hw, dev)
+            bufs = []
+            for st in self.steps:
+                ho = st.h // 2 if st.pool else st.h
+                bufs.append(device.halo_empty(n, st.k, ho, ho, dev))
+            self._bufs, self._bufs_batch = bufs, n
+        return self._bufs
+
+    @property
+    def launches_per_forward(self) -> int:
+        return len(self.steps)
+
+    def stage_input(self, x: torch.Tensor) -> torch.Tensor:
+        """Copy a dense [N, C, H, W] CUDA batch into the engine's halo input buffer."""
+        self._buffers(int(x.shape[0]))
+        self._in[..., 1 : self.hw + 1].copy_(x)
+        return self._in
+
+    def run(self, xh: torch.Tensor) -> torch.Tensor:
+        """Run the stack on a halo-layout input; returns the halo output buffer."""
+        bufs = self._buffers(int(xh.shape[0]))
+        cur, w = xh, self.hw
+        for st, out in zip(self.steps, bufs):
+            device.sf_conv3x3(cur, st.bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly)
+            cur = out
+            w = w // 2 if st.pool else w
+        return cur
+
+    def forward_device(self, x: torch.Tensor) -> torch.Tensor:
+        """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer)."""
+        assert x.shape[1] == self.in_c and x.shape[2] == self.hw and x.shape[3] == self.hw
+        y = self.run(self.stage_input(x))
+        return device.from_halo(y, self.out_hw)
+
+    def flops_per_image(self) -> int:
+        """Exact nnz-FLOPs per image: 2 x in-bounds multiplies (kernels.py:108-133)."""
+        total = 0
+        for st in self.steps:
+            seg = st.seg_off.cpu().numpy().reshape(st.k, 9)
+            ends = np.append(seg.ravel()[1:], st.n_nodes).reshape(st.k, 9)
+            nnz_tap = (ends - seg - 1).sum(axis=0)  # per tap index kw*3 + kh
+            for tap in range(9):
+                l, kk = divmod(tap, 3)  # reference segment order: kw outer, kh inner
+                rows = sum(1 for i in range(st.h) if 0 <= kk + i - 1 < st.h)
+                cols = sum(1 for j in range(st.w) if 0 <= l + j - 1 < st.w)
+                total += int(nnz_tap[tap]) * rows * cols
+        return 2 * total
+
+    def bytes_per_image(self) -> int:
+        """Compulsory HBM bytes per image: each conv reads its input and writes its
+        (pooled) output once; filter streams are amortised over the batch (counted once
+        per batch by callers)."""
+        b = 0
+        for st in self.steps:
+            ho = st.h // 2 if st.pool else st.h
+            b += 4 * (st.c * st.h * st.w + st.k * ho * ho)
+        return b
+
+    def filter_bytes(self) -> int:
+        return sum(st.bank.total * 8 + st.bank.seg_off.numel() * 8 for st in self.steps)
