@@ -107,7 +107,8 @@ int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_
  * accumulation order).  Consumes the kernel-side packed filter stream:
  *   the filter bank regrouped into groups of `kt` filters; for group g and input
  *   channel c, segment g*c_n + c lists the nonzeros W[g*kt + kl][c][kh][kw] as
- *   nodes with index = kl*9 + kh*3 + kw, ascending, sentinel-terminated.
+ *   nodes with index = kl*9 + kh*3 + kw, ascending, terminated by a sentinel whose
+ *   index is kt*9 (the kernel jump table's exit target) rather than -1.
  * Build it with fscnn_sf_pack_offsets / fscnn_sf_pack_nodes from a dense
  * [K][C][3][3] bank (itself decoded from the reference's CHW SparseTensor4 by
  * fscnn_decode, or straight from dense weights).

@@ -85,7 +85,8 @@ __global__ void count_warp_kernel(Src src, int64_t n_seg, int64_t *cnt) {
 }
 
 template <class Src>
-__global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes) {
+__global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes,
+                                    int sentinel) {
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= n_seg) return;
     auto b = src.fiber(s);
@@ -94,11 +95,12 @@ __global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_o
         float v = src.at(b, i);
         if (v != 0.0f) nodes[p++] = make_int2((int)i, __float_as_int(v));
     }
-    nodes[p] = make_int2(-1, 0);
+    nodes[p] = make_int2(sentinel, 0);
 }
 
 template <class Src>
-__global__ void write_warp_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes) {
+__global__ void write_warp_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes,
+                                  int sentinel) {
     int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (s >= n_seg) return;
@@ -113,7 +115,7 @@ __global__ void write_warp_kernel(Src src, int64_t n_seg, const int64_t *seg_off
         if (nz) nodes[p + __popc(m & lt)] = make_int2((int)i, __float_as_int(v));
         p += __popc(m);
     }
-    if (lane == 0) nodes[p] = make_int2(-1, 0);
+    if (lane == 0) nodes[p] = make_int2(sentinel, 0);
 }
 
 // --- int64 exclusive scan -------------------------------------------------------
@@ -241,14 +243,14 @@ int encode_offsets_impl(const Src &src, int64_t n_seg, bool warp_mode, int64_t *
 
 template <class Src>
 int encode_nodes_impl(const Src &src, int64_t n_seg, bool warp_mode, const int64_t *seg_off,
-                      fscnn_node *nodes, cudaStream_t st) {
+                      fscnn_node *nodes, cudaStream_t st, int sentinel = -1) {
     if (n_seg == 0) return FSCNN_OK;
     int2 *out = reinterpret_cast<int2 *>(nodes);
     if (warp_mode) {
-        write_warp_kernel<<<(unsigned)ceil_div(n_seg * 32, 256), 256, 0, st>>>(src, n_seg, seg_off, out);
+        write_warp_kernel<<<(unsigned)ceil_div(n_seg * 32, 256), 256, 0, st>>>(src, n_seg, seg_off, out, sentinel);
         FSCNN_LAUNCH_CHECK("write_warp_kernel");
     } else {
-        write_thread_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(src, n_seg, seg_off, out);
+        write_thread_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(src, n_seg, seg_off, out, sentinel);
         FSCNN_LAUNCH_CHECK("write_thread_kernel");
     }
     return FSCNN_OK;
@@ -353,7 +355,8 @@ int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, const int64_t *seg_of
     FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && nodes, "bad pack arguments");
     int64_t groups = ceil_div(k, kSfPackKt);
     SfPackSrc src{w_kc33, k, c, kSfPackKt, kSfPackKt * 9};
-    return encode_nodes_impl(src, groups * c, false, seg_off, nodes, as_stream(stream));
+    // the fast kernel's jump table maps index kt*9 to its loop exit: that is the sentinel
+    return encode_nodes_impl(src, groups * c, false, seg_off, nodes, as_stream(stream), kSfPackKt * 9);
 }
 
 }  // extern "C"

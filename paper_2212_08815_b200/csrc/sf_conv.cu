@@ -70,7 +70,7 @@ __global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, i
 constexpr int KT = 4 * 2;          // filters per warp group (must match fscnn_sf_pack_kt)
 constexpr int NWARP = 8;           // consumer warps per CTA -> 64 filters per CTA
 constexpr int NTHREADS = NWARP * 32;         // warp 0 lane 0 doubles as the TMA producer
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
 constexpr int TILE = 4;            // lane tile is TILE x TILE outputs
 constexpr int SUBW = 16;           // sub-region width (4 lanes x 4 columns)
@@ -146,7 +146,7 @@ struct Sf3Params {
     int dbg;                  // debug: 1 = walk entries without FMAs, 3 = no TMA, 4 = no bulk copies
 };
 
-template <int LY>
+template <int LY, bool THREADED>
 __global__ void __launch_bounds__(NTHREADS, 1)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
     constexpr int LI = 8 / LY;          // sub-regions per CTA
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int2 *ent_s = reinterpret_cast<int2 *>(in_s + STAGES * stage_in_floats);
     uint64_t *full = reinterpret_cast<uint64_t *>(ent_s + STAGES * NWARP * p.ent_cap);
     uint64_t *empty = full + STAGES;
+    int *cofs = reinterpret_cast<int *>(empty + STAGES);  // [NWARP][n_chunks + 1] run starts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub0 = blockIdx.x * LI;
@@ -165,6 +166,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int n_groups = (p.k + KT - 1) / KT;
     const int n_chunks = (p.c + p.cc - 1) / p.cc;
 
+    // chunk-run table: cofs[w][j] = first packed node of group g0+w, channel j*cc
+    // (j = n_chunks: one past the group's last node) -- keeps global loads off the loop
+    for (int idx = threadIdx.x; idx < NWARP * (n_chunks + 1); idx += NTHREADS) {
+        const int wv = idx / (n_chunks + 1), j = idx % (n_chunks + 1);
+        const int gg = g0 + wv;
+        int64_t v = 0;
+        if (gg < n_groups) {
+            if (j < n_chunks) v = p.seg_off[(int64_t)gg * p.c + (int64_t)j * p.cc];
+            else v = (gg + 1 < n_groups) ? p.seg_off[(int64_t)(gg + 1) * p.c] : p.total_nodes;
+        }
+        cofs[idx] = (int)v;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -178,8 +191,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // Producer: fill one stage with chunk `ch` (TMA boxes + the 8 warps' entry runs).
     auto produce = [&](int ch) {
         const int s = ch % STAGES;
-        const int c0 = ch * p.cc;
-        const int cnt = min(p.cc, p.c - c0);
         uint32_t bytes = 0;
         int64_t lo[NWARP], len16[NWARP];
 #pragma unroll
@@ -188,9 +199,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             lo[wv] = 0;
             len16[wv] = 0;
             if (g < n_groups) {
-                int64_t a = p.seg_off[(int64_t)g * p.c + c0];
-                int64_t sidx = (int64_t)g * p.c + c0 + cnt;
-                int64_t b = (sidx < (int64_t)n_groups * p.c) ? p.seg_off[sidx] : p.total_nodes;
+                int64_t a = cofs[wv * (n_chunks + 1) + ch];
+                int64_t b = cofs[wv * (n_chunks + 1) + ch + 1];
                 int64_t a2 = a & ~int64_t(1);  // 16-byte aligned start
                 int64_t nb = ((b - a2) * 8 + 15) & ~int64_t(15);
                 lo[wv] = a2;
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // memory cols tw*SUBW .. +19 of the halo-column layout (16-byte aligned start:
             // the TMA unit faults on a misaligned innermost coordinate)
             tma_load_4d(in_s + s * stage_in_floats + li * p.box_floats, &tmap, &full[s],
-                        tw * SUBW, th * SUBH - 1, c0, img);
+                        tw * SUBW, th * SUBH - 1, ch * p.cc, img);
         }
     };
     const bool producer = (threadIdx.x == 0);
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int cnt = min(p.cc, p.c - c0);
         if (g < n_groups) {
             const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
-            const int e0 = (int)(p.seg_off[(int64_t)g * p.c + c0] & 1);  // offset inside aligned copy
+            const int e0 = cofs[warp * (n_chunks + 1) + ch] & 1;  // offset inside aligned copy
             uint32_t cur = smem_u32(ents + e0);
             const float *box = in_s + s * stage_in_floats + li * p.box_floats;
             for (int cc = 0; cc < cnt; ++cc) {
@@ -266,12 +276,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (p.dbg >= 3) {
                     // garbage entries: do not walk them
                 } else if (p.dbg == 0) {
-                    cur = sf3x3_channel(acc, pt, cur);
+                    cur = THREADED ? sf3x3_channel_threaded(acc, pt, cur) : sf3x3_channel_looped(acc, pt, cur);
                 } else {
                     const int2 *ep = reinterpret_cast<const int2 *>(ents) + ((cur - smem_u32(ents)) >> 3);
                     for (;;) {
                         const int2 en = *ep++;
-                        if (en.x < 0) break;
+                        if (en.x < 0 || en.x >= KT * 9) break;
                     }
                     cur = smem_u32(ep);
                 }
@@ -374,7 +384,7 @@ EncodeTiledFn get_encode_tiled() {
     return fn;
 }
 
-template <int LY>
+template <int LY, bool THREADED>
 int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     constexpr int LI = 8 / LY;
     constexpr int SUBH = TILE * LY;
@@ -384,13 +394,14 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     p.box_floats = BOXW * (SUBH + 2) * p.cc;
     // each box must start 128-byte aligned (TMA destination)
     p.box_floats = (p.box_floats + 31) & ~31;
+    const int n_chunks = (int)ceil_div(p.c, p.cc);
     size_t smem = (size_t)STAGES * LI * p.box_floats * 4 + (size_t)STAGES * NWARP * p.ent_cap * 8 +
-                  2 * STAGES * 8;
+                  2 * STAGES * 8 + (size_t)NWARP * (n_chunks + 1) * 4;
     if (smem > 227 * 1024) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
         return FSCNN_ERR_UNSUPPORTED;
     }
-    auto kern = sf3x3_kernel<LY>;
+    auto kern = sf3x3_kernel<LY, THREADED>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("sf3x3: smem attribute (%zu bytes): %s", smem, cudaGetErrorString(e));
@@ -476,10 +487,14 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
         return FSCNN_ERR_CUDA;
     }
     cudaStream_t st = as_stream(stream);
-    switch (ly) {
-        case 8: return launch_sf3x3<8>(map, p, st);
-        case 4: return launch_sf3x3<4>(map, p, st);
-        case 2: return launch_sf3x3<2>(map, p, st);
+    static const int threaded = getenv("FSCNN_SF3_THREADED") ? atoi(getenv("FSCNN_SF3_THREADED")) : 0;
+    switch (ly * 2 + (threaded ? 1 : 0)) {
+        case 17: return launch_sf3x3<8, true>(map, p, st);
+        case 9: return launch_sf3x3<4, true>(map, p, st);
+        case 5: return launch_sf3x3<2, true>(map, p, st);
+        case 16: return launch_sf3x3<8, false>(map, p, st);
+        case 8: return launch_sf3x3<4, false>(map, p, st);
+        case 4: return launch_sf3x3<2, false>(map, p, st);
         default: set_error("unsupported sub-region height %d", ly); return FSCNN_ERR_ARG;
     }
 }

@@ -136,7 +136,7 @@ def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None
 
 # -- sparse-filter conv ------------------------------------------------------------------
 
-STAGES, NWARP, BOXW, SUBW, TILE = 3, 8, 20, 16, 4
+STAGES, NWARP, BOXW, SUBW, TILE = 4, 8, 20, 16, 4
 SMEM_LIMIT = 227 * 1024
 
 
@@ -144,10 +144,12 @@ def _align(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int) -> int:
+def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int) -> int:
     li = 8 // ly
     box = _align(BOXW * (TILE * ly + 2) * cc, 32)
-    return STAGES * li * box * 4 + STAGES * NWARP * ent_cap * 8 + 2 * STAGES * 8
+    n_chunks = math.ceil(c / cc)
+    return (STAGES * li * box * 4 + STAGES * NWARP * ent_cap * 8 + 2 * STAGES * 8
+            + NWARP * (n_chunks + 1) * 4)
 
 
 def pick_ly(h: int) -> int:
@@ -188,7 +190,7 @@ class PackedBank:
             cnt = np.pad(self.counts, ((0, 0), (0, pad)))
             mx = int(cnt.reshape(cnt.shape[0], n_chunks, cc).sum(axis=2).max())
             ent_cap = (mx + 4) & ~1
-            if sf3x3_smem_bytes(ly, cc, ent_cap) <= SMEM_LIMIT:
+            if sf3x3_smem_bytes(ly, cc, ent_cap, self.c) <= SMEM_LIMIT:
                 self._cache[ly] = (cc, mx)
                 return cc, mx
         raise RuntimeError("filter bank too dense for the fast kernel's shared memory")
