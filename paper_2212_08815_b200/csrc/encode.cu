@@ -277,7 +277,7 @@ __global__ void decode_kernel(const int2 *nodes, const int64_t *seg_off, int64_t
     }
 }
 
-constexpr int kSfPackKt = 8;  // must match KT in sf_conv.cu
+constexpr int kSfPackKt = 4;  // must match KT (FSCNN_SF3_KT) in sf_conv.cu
 
 }  // namespace
 

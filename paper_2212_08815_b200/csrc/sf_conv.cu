@@ -27,6 +27,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "sf3x3_dispatch.inc"
 
 namespace fscnn {
 namespace {
@@ -67,15 +68,14 @@ __global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, i
 // ------------------------------------------------------------------------------
 // fast 3x3 kernel
 // ------------------------------------------------------------------------------
-constexpr int KT = 4 * 2;          // filters per warp group (must match fscnn_sf_pack_kt)
-constexpr int NWARP = 8;           // consumer warps per CTA -> 64 filters per CTA
+constexpr int KT = FSCNN_SF3_KT;   // filters per warp group (== fscnn_sf_pack_kt)
+constexpr int NWARP = 8;           // warps per CTA -> 32 filters per CTA; 2 CTAs per SM
 constexpr int NTHREADS = NWARP * 32;         // warp 0 lane 0 doubles as the TMA producer
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 4;
 constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
 constexpr int TILE = 4;            // lane tile is TILE x TILE outputs
 constexpr int SUBW = 16;           // sub-region width (4 lanes x 4 columns)
 
-static_assert(KT == 8, "switch below is written for 8 filters per group");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -125,8 +125,6 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
         : "memory");
 }
 
-#include "sf3x3_dispatch.inc"
-
 struct Sf3Params {
     const int2 *packed;       // packed filter stream (+16 B slack at the end)
     const int64_t *seg_off;   // [groups][C] segment offsets
@@ -143,17 +141,19 @@ struct Sf3Params {
     float *y;
     int relu;
     int pool;                 // fused 2x2 max-pool
+    int stages;               // ring depth (<= MAX_STAGES)
     int dbg;                  // debug: 1 = walk entries without FMAs, 3 = no TMA, 4 = no bulk copies
 };
 
 template <int LY, bool THREADED>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, 2)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
     constexpr int LI = 8 / LY;          // sub-regions per CTA
     constexpr int SUBH = TILE * LY;     // sub-region height
     constexpr int BOXH = SUBH + 2;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float *in_s = reinterpret_cast<float *>(smem_raw);
+    const int STAGES = p.stages;
     const int stage_in_floats = LI * p.box_floats;
     int2 *ent_s = reinterpret_cast<int2 *>(in_s + STAGES * stage_in_floats);
     uint64_t *full = reinterpret_cast<uint64_t *>(ent_s + STAGES * NWARP * p.ent_cap);
@@ -191,22 +191,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // Producer: fill one stage with chunk `ch` (TMA boxes + the 8 warps' entry runs).
     auto produce = [&](int ch) {
         const int s = ch % STAGES;
+        // entry run of warp wv for this chunk: [a2, b) rounded to 16-byte units
+        auto run = [&](int wv, int &lo, uint32_t &nbytes) {
+            const int a = cofs[wv * (n_chunks + 1) + ch];
+            const int b = cofs[wv * (n_chunks + 1) + ch + 1];
+            lo = a & ~1;
+            nbytes = (uint32_t)(((b - lo) * 8 + 15) & ~15);
+        };
         uint32_t bytes = 0;
-        int64_t lo[NWARP], len16[NWARP];
-#pragma unroll
         for (int wv = 0; wv < NWARP; ++wv) {
-            int g = g0 + wv;
-            lo[wv] = 0;
-            len16[wv] = 0;
-            if (g < n_groups) {
-                int64_t a = cofs[wv * (n_chunks + 1) + ch];
-                int64_t b = cofs[wv * (n_chunks + 1) + ch + 1];
-                int64_t a2 = a & ~int64_t(1);  // 16-byte aligned start
-                int64_t nb = ((b - a2) * 8 + 15) & ~int64_t(15);
-                lo[wv] = a2;
-                len16[wv] = nb;
-                if (p.dbg != 4) bytes += (uint32_t)nb;
-            }
+            if (g0 + wv >= n_groups) break;
+            int lo; uint32_t nb;
+            run(wv, lo, nb);
+            if (p.dbg != 4) bytes += nb;
         }
         int n_box = 0;
 #pragma unroll
@@ -214,11 +211,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // a box always moves cc channels (OOB ones zero-filled) and counts them all
         if (p.dbg != 3) bytes += (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
         mbar_expect_tx(&full[s], bytes);
-#pragma unroll
-        for (int wv = 0; wv < NWARP; ++wv)
-            if (len16[wv] > 0 && p.dbg != 4)
-                bulk_load(ent_s + (s * NWARP + wv) * p.ent_cap, p.packed + lo[wv],
-                          (uint32_t)len16[wv], &full[s]);
+        for (int wv = 0; wv < NWARP && p.dbg != 4; ++wv) {
+            if (g0 + wv >= n_groups) break;
+            int lo; uint32_t nb;
+            run(wv, lo, nb);
+            bulk_load(ent_s + (s * NWARP + wv) * p.ent_cap, p.packed + lo, nb, &full[s]);
+        }
 #pragma unroll
         for (int li = 0; li < LI; ++li) {
             int sub = sub0 + li;
@@ -395,8 +393,14 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     // each box must start 128-byte aligned (TMA destination)
     p.box_floats = (p.box_floats + 31) & ~31;
     const int n_chunks = (int)ceil_div(p.c, p.cc);
-    size_t smem = (size_t)STAGES * LI * p.box_floats * 4 + (size_t)STAGES * NWARP * p.ent_cap * 8 +
-                  2 * STAGES * 8 + (size_t)NWARP * (n_chunks + 1) * 4;
+    auto smem_for = [&](int st) {
+        return (size_t)st * LI * p.box_floats * 4 + (size_t)st * NWARP * p.ent_cap * 8 + 2 * st * 8 +
+               (size_t)NWARP * (n_chunks + 1) * 4;
+    };
+    // deepest ring that still lets two CTAs share an SM (228 KB, 1 KB reserved each)
+    p.stages = MAX_STAGES;
+    while (p.stages > 2 && smem_for(p.stages) > 113 * 1024) --p.stages;
+    size_t smem = smem_for(p.stages);
     if (smem > 227 * 1024) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
         return FSCNN_ERR_UNSUPPORTED;

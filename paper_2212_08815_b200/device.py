@@ -136,7 +136,7 @@ def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None
 
 # -- sparse-filter conv ------------------------------------------------------------------
 
-STAGES, NWARP, BOXW, SUBW, TILE = 4, 8, 20, 16, 4
+STAGES, NWARP, BOXW, SUBW, TILE = 2, 8, 20, 16, 4  # STAGES: the minimum ring the kernel runs with
 SMEM_LIMIT = 227 * 1024
 
 
