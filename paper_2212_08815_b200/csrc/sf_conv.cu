@@ -14,8 +14,10 @@
 //      * input channels stream through shared memory in chunks of CC channels: one
 //        TMA box per sub-region per chunk ((4LY+2) x 20 floats x CC, zero fill for
 //        the conv padding) plus a bulk copy of each warp's packed nonzero list for
-//        those channels, completed on an mbarrier (S-stage ring, dedicated producer
-//        warp, per-stage empty barriers so warps drift instead of lock-stepping);
+//        those channels, completed on an mbarrier (S-stage ring).  There is no
+//        producer warp: each warp restages its own entry run as soon as it leaves a
+//        stage, and the last warp to leave (smem counter) restages the shared boxes,
+//        so warps drift freely within the ring instead of waiting for a producer;
 //      * per channel a lane loads its 6x6 input patch into registers (12 x LDS.128,
 //        conflict-free with the 20-float row pitch), then walks the warp-uniform
 //        nonzero list (kl, tap, value); a switch dispatches each nonzero to 16
@@ -157,8 +159,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     const int stage_in_floats = LI * p.box_floats;
     int2 *ent_s = reinterpret_cast<int2 *>(in_s + STAGES * stage_in_floats);
     uint64_t *full = reinterpret_cast<uint64_t *>(ent_s + STAGES * NWARP * p.ent_cap);
-    uint64_t *empty = full + STAGES;
-    int *cofs = reinterpret_cast<int *>(empty + STAGES);  // [NWARP][n_chunks + 1] run starts
+    int *done = reinterpret_cast<int *>(full + STAGES);    // per-stage finished-warp counters
+    int *cofs = done + 2 * STAGES;                           // [NWARP][n_chunks + 1] run starts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub0 = blockIdx.x * LI;
@@ -180,67 +182,68 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NWARP);
+            // NWARP entry-run arrivals + 1 input-box arrival complete a stage
+            mbar_init(&full[s], NWARP + 1);
+            done[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
     __syncthreads();
 
-    // Producer: fill one stage with chunk `ch` (TMA boxes + the 8 warps' entry runs).
-    auto produce = [&](int ch) {
-        const int s = ch % STAGES;
-        // entry run of warp wv for this chunk: [a2, b) rounded to 16-byte units
-        auto run = [&](int wv, int &lo, uint32_t &nbytes) {
-            const int a = cofs[wv * (n_chunks + 1) + ch];
-            const int b = cofs[wv * (n_chunks + 1) + ch + 1];
-            lo = a & ~1;
-            nbytes = (uint32_t)(((b - lo) * 8 + 15) & ~15);
-        };
-        uint32_t bytes = 0;
-        for (int wv = 0; wv < NWARP; ++wv) {
-            if (g0 + wv >= n_groups) break;
-            int lo; uint32_t nb;
-            run(wv, lo, nb);
-            if (p.dbg != 4) bytes += nb;
-        }
-        int n_box = 0;
+    const int g = g0 + warp;
+    const bool live = g < n_groups;
+    int n_box = 0;
 #pragma unroll
-        for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
-        // a box always moves cc channels (OOB ones zero-filled) and counts them all
-        if (p.dbg != 3) bytes += (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
-        mbar_expect_tx(&full[s], bytes);
-        for (int wv = 0; wv < NWARP && p.dbg != 4; ++wv) {
-            if (g0 + wv >= n_groups) break;
-            int lo; uint32_t nb;
-            run(wv, lo, nb);
-            bulk_load(ent_s + (s * NWARP + wv) * p.ent_cap, p.packed + lo, nb, &full[s]);
+    for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
+    const uint32_t box_bytes =
+        (p.dbg == 3) ? 0u : (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
+
+    // Each warp stages its own entry run for chunk ch (lane 0); dead groups arrive empty.
+    auto refill_entries = [&](int ch) {
+        const int s = ch % STAGES;
+        uint32_t nb = 0;
+        int lo = 0;
+        if (live && p.dbg != 4) {
+            const int a = cofs[warp * (n_chunks + 1) + ch];
+            const int b = cofs[warp * (n_chunks + 1) + ch + 1];
+            lo = a & ~1;  // 16-byte aligned start
+            nb = (uint32_t)(((b - lo) * 8 + 15) & ~15);
         }
+        mbar_expect_tx(&full[s], nb);
+        if (nb) bulk_load(ent_s + (s * NWARP + warp) * p.ent_cap, p.packed + lo, nb, &full[s]);
+    };
+    // The shared input boxes of chunk ch (the TMA zero-fills the conv padding).
+    auto refill_boxes = [&](int ch) {
+        const int s = ch % STAGES;
+        mbar_expect_tx(&full[s], box_bytes);
+        if (p.dbg == 3) return;
 #pragma unroll
         for (int li = 0; li < LI; ++li) {
             int sub = sub0 + li;
-            if (sub >= p.n_sub || p.dbg == 3) continue;
+            if (sub >= p.n_sub) continue;
             int tw = sub % p.tiles_w;
             int r = sub / p.tiles_w;
             int th = r % p.tiles_h;
             int img = r / p.tiles_h;
-            // box covers rows th*SUBH-1 .. +SUBH and logical cols tw*SUBW-1 .. +18, i.e.
-            // memory cols tw*SUBW .. +19 of the halo-column layout (16-byte aligned start:
-            // the TMA unit faults on a misaligned innermost coordinate)
+            // rows th*SUBH-1 .. +SUBH and logical cols tw*SUBW-1 .. +18 = memory cols
+            // tw*SUBW .. +19 of the halo-column layout (16-byte aligned innermost start:
+            // the TMA unit faults on a misaligned one)
             tma_load_4d(in_s + s * stage_in_floats + li * p.box_floats, &tmap, &full[s],
                         tw * SUBW, th * SUBH - 1, ch * p.cc, img);
         }
     };
-    const bool producer = (threadIdx.x == 0);
-    if (producer)
-        for (int ch = 0; ch < STAGES && ch < n_chunks; ++ch) produce(ch);
+
+    if (lane == 0)
+        for (int ch = 0; ch < STAGES && ch < n_chunks; ++ch) {
+            refill_entries(ch);
+            if (warp == 0) refill_boxes(ch);
+        }
     __syncwarp();  // the dispatch loop's .uni branches need a converged warp
 
     const int lx = lane & 3;
     const int ly = (lane >> 2) % LY;
     const int li = lane / (4 * LY);
-    const int g = g0 + warp;
 
     float acc[KT][TILE][TILE];
 #pragma unroll
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         __syncwarp();
         const int c0 = ch * p.cc;
         const int cnt = min(p.cc, p.c - c0);
-        if (g < n_groups) {
+        if (live) {
             const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
             const int e0 = cofs[warp * (n_chunks + 1) + ch] & 1;  // offset inside aligned copy
             uint32_t cur = smem_u32(ents + e0);
@@ -286,16 +289,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        // Refill the stage consumed one chunk ago (prefetch distance STAGES-1), once
-        // every warp has released it; by then it is usually already free.
-        if (producer && ch >= 1) {
-            const int prev = ch - 1;
-            const int nxt = prev + STAGES;
-            if (nxt < n_chunks) {
-                mbar_wait(&empty[prev % STAGES], (prev / STAGES) & 1);
-                produce(nxt);
-            }
+        // Stage s is free for this warp: restage its own entry run for chunk ch+STAGES;
+        // the last warp to leave the stage also restages the shared input boxes.
+        if (lane == 0 && ch + STAGES < n_chunks) {
+            refill_entries(ch + STAGES);
+            // the counter only grows: every NWARP-th arrival closes a round
+            if ((atomicAdd(&done[s], 1) + 1) % NWARP == 0) refill_boxes(ch + STAGES);
         }
         __syncwarp();
     }

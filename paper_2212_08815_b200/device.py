@@ -182,8 +182,11 @@ class PackedBank:
             self._cache = {}
         if ly in self._cache:
             return self._cache[ly]
-        for cc in (8, 4, 2, 1):
-            if cc > self.c and cc != 1:
+        import os
+
+        forced = int(os.environ.get("FSCNN_SF3_CC", "0"))
+        for cc in ((forced,) if forced else (8, 4, 2, 1)):
+            if cc > self.c and cc != 1 and not forced:
                 continue
             n_chunks = math.ceil(self.c / cc)
             pad = n_chunks * cc - self.c
