@@ -1,0 +1,252 @@
+"""The drop-in API (mirror of sparse_infer's hot-path surface) on the GPU, checked the
+way the reference's own tests check the reference (pkg/tests/test_sparse_core.py,
+test_kernels.py, test_layers.py, test_network.py), against its golden outputs and
+the oracle.
+
+Tolerances: bit-exact wherever the reference contract is (encoder/decoder, the
+reference-order kernels, SI layer nodes, pooling, strategy I == II, worker and batch
+invariance); the fast 3x3 path is held to north_star's max|err| <= 1e-4 max|ref|.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, nodes_from_i64, normwise_err
+
+import paper_2212_08815_b200 as fs
+from paper_2212_08815_b200 import network as nw, workloads as wl
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _fast_kernels():
+    fs.set_exact(False)
+    yield
+    fs.set_exact(False)
+
+
+def test_encoder_api_all_orders_bitwise():
+    g = load_golden("encoder.npz")
+    for name in g["names"]:
+        name = str(name)
+        arr = g[f"{name}__input"]
+        order = fs.AxisOrder3[str(g[f"{name}__order"])]
+        t = fs.sparsify_tensor3(fs.DenseTensor3.from_array(arr), order)
+        t.validate()
+        assert t.nodes.view(np.int64).tobytes() == g[f"{name}__nodes"].tobytes(), name
+        assert np.array_equal(t.segment_offsets, g[f"{name}__segment_offsets"]), name
+        back = fs.densify_tensor3(t)
+        want = np.where(arr == 0, np.float32(0), arr)
+        assert np.array_equal(back.to_array(), want, equal_nan=True), name
+
+
+def test_encoder_known_answers():
+    z = fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.zeros((2, 2, 2), np.float32)), fs.AxisOrder3.CHW)
+    assert z.nnz == 0 and len(z.nodes) == 4 and len(z.segment_offsets) == 4
+    o = fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.ones((2, 2, 2), np.float32)), fs.AxisOrder3.CHW)
+    for k in range(4):
+        s = o.segment_offsets[k]
+        assert list(o.nodes["index"][s : s + 3]) == [0, 1, -1]
+    with pytest.raises(fs.FormatError):
+        fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.zeros((1, 1, 1), np.float32)), "chw")
+
+
+def test_round_trip_random_tensors_bitwise():
+    rng = np.random.default_rng(11)
+    for _ in range(60):
+        dims = tuple(int(x) for x in rng.integers(1, 9, 3))
+        arr = rng.uniform(-0.5, 0.5, dims).astype(np.float32)
+        arr[rng.random(dims) >= 0.1] = 0
+        order = fs.AxisOrder3(int(rng.integers(0, 6)))
+        t = fs.DenseTensor3.from_array(arr)
+        s = fs.sparsify_tensor3(t, order)
+        assert np.array_equal(fs.densify_tensor3(s).data, t.data)
+
+
+def test_matrix_round_trip():
+    rng = np.random.default_rng(17)
+    arr = rng.uniform(-1, 1, (6, 9)).astype(np.float32)
+    arr[rng.random(arr.shape) > 0.3] = 0.0
+    for order in fs.AxisOrder2:
+        m = fs.sparsify_matrix(arr, order)
+        m.validate()
+        assert np.array_equal(fs.densify_matrix(m), arr)
+
+
+def _golden_bank(w):
+    return fs.SparseTensor4.stack([fs.sparsify_tensor3(fs.DenseTensor3.from_array(f), fs.AxisOrder3.CHW) for f in w])
+
+
+def test_sparse_filter_layers_match_reference():
+    g = load_golden("sf_conv.npz")
+    for i in range(int(g["n_cases"])):
+        x, w, bias, y = g[f"c{i}__x"], g[f"c{i}__w"], g[f"c{i}__bias"], g[f"c{i}__y"]
+        s, p = (int(v) for v in g[f"c{i}__geom"])
+        t4 = _golden_bank(w)
+        t_in = fs.DenseTensor3.from_array(x)
+        a = fs.conv_forward_strategy_I(t_in, t4, s, p, bias)
+        b = fs.conv_forward_strategy_II(t_in, t4, s, p, bias)
+        assert a.dims == b.dims and np.array_equal(a.data, b.data), i  # strategies bit-equal
+        fast = w.shape[2:] == (3, 3) and (s, p) == (1, 1)
+        if fast:
+            assert normwise_err(a.to_array(), y) <= TOL, i
+        else:
+            assert np.array_equal(a.to_array().view(np.int32), y.view(np.int32)), i
+        fs.set_exact(True)
+        e = fs.conv_forward_strategy_II(t_in, t4, s, p, bias)
+        fs.set_exact(False)
+        assert np.array_equal(e.to_array().view(np.int32), y.view(np.int32)), i
+
+
+def test_single_filter_kernels_and_counted():
+    g = load_golden("sf_conv.npz")
+    for i in range(0, int(g["n_cases"]), 3):
+        x, w, y = g[f"c{i}__x"], g[f"c{i}__w"], g[f"c{i}__y"]
+        s, p = (int(v) for v in g[f"c{i}__geom"])
+        bias = g[f"c{i}__bias"]
+        t_in = fs.DenseTensor3.from_array(x)
+        geom = fs.ConvGeometry(t_in.dims, w.shape[1:], s, p)
+        total = 0
+        for f in range(w.shape[0]):
+            t_f = fs.sparsify_tensor3(fs.DenseTensor3.from_array(w[f]), fs.AxisOrder3.CHW)
+            plain = fs.conv_dense_input_sparse_filter(t_in, t_f, geom)
+            counted, n = fs.conv_dense_input_sparse_filter_counted(t_in, t_f, geom)
+            assert np.array_equal(plain, counted)
+            # per-filter plane + bias == layer output (same order, same roundings)
+            assert np.array_equal((plain + bias[f]).view(np.int32), y[f].view(np.int32)), (i, f)
+            total += n
+        assert total == int(g[f"c{i}__mults"])
+    with pytest.raises(fs.FormatError, match="CHW"):
+        t_f = fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.ones((1, 1, 1), np.float32)), fs.AxisOrder3.WHC)
+        fs.conv_dense_input_sparse_filter(fs.DenseTensor3.from_array(np.ones((1, 3, 3), np.float32)), t_f,
+                                          fs.ConvGeometry((1, 3, 3), (1, 1, 1)))
+
+
+def test_sparse_input_layer_matches_reference_bitwise():
+    g = load_golden("si_conv.npz")
+    for i in range(int(g["n_cases"])):
+        x, w, bias, y = g[f"c{i}__x"], g[f"c{i}__w"], g[f"c{i}__bias"], g[f"c{i}__y"]
+        s, p = (int(v) for v in g[f"c{i}__geom"])
+        sp = fs.sparsify_tensor3(fs.DenseTensor3.from_array(x), fs.AxisOrder3.CHW)
+        filters = [fs.DenseTensor3.from_array(f) for f in w]
+        out = fs.conv_forward_sparse_input(sp, filters, s, p, bias)
+        if str(g[f"c{i}__kind"]) == "dense":
+            assert isinstance(out, fs.DenseTensor3)
+            assert np.array_equal(out.to_array(), y), i
+        else:
+            assert isinstance(out, fs.SparseTensor3)
+            assert out.nodes.view(np.int64).tobytes() == g[f"c{i}__nodes"].tobytes(), i
+            assert np.array_equal(out.segment_offsets, g[f"c{i}__segment_offsets"]), i
+            geom = fs.ConvGeometry(sp.dims, filters[0].dims, s, p)
+            m = fs.conv_sparse_input_dense_filter(sp, filters[0], geom)
+            m.validate()
+            assert np.array_equal(fs.densify_matrix(m), y[0]), i
+
+
+def test_fusion_equals_unfused_exactly():
+    rng = np.random.default_rng(56)
+    for mode in ("max", "avg"):
+        x = rng.uniform(-0.5, 0.5, (3, 8, 8)).astype(np.float32)
+        x[rng.random(x.shape) >= 0.3] = 0
+        sp = fs.sparsify_tensor3(fs.DenseTensor3.from_array(x), fs.AxisOrder3.CHW)
+        f = fs.DenseTensor3.from_array(rng.normal(0, 0.3, (3, 3, 3)).astype(np.float32))
+        fused = fs.merged_conv_pool(sp, f, 1, (2, 2), mode, padding=1)
+        conv = fs.conv_sparse_input_dense_filter(sp, f, fs.ConvGeometry((3, 8, 8), (3, 3, 3), 1, 1))
+        pooled = fs.pool_standalone(fs.DenseTensor3.from_array(fs.densify_matrix(conv)[None]), (2, 2), mode)
+        assert np.array_equal(fs.densify_matrix(fused), pooled.to_array()[0])
+        zb = np.zeros(4, np.float32)
+        filters = [fs.DenseTensor3.from_array(rng.normal(0, 0.3, (3, 3, 3)).astype(np.float32)) for _ in range(4)]
+        a = fs.conv_forward_sparse_input(sp, filters, 1, 1, zb, fused_pool=(2, 2), pool_mode=mode)
+        b = fs.conv_forward_sparse_input(sp, filters, 1, 1, zb)
+        bp = fs.pool_standalone(fs.densify_tensor3(b), (2, 2), mode)
+        assert np.array_equal(fs.densify_tensor3(a).data, bp.data)
+
+
+def test_pool_and_relu_api():
+    g = load_golden("pool_relu.npz")
+    for i in range(4):
+        x, y = g[f"p{i}__x"], g[f"p{i}__y"]
+        got = fs.pool_standalone(fs.DenseTensor3.from_array(x), tuple(int(v) for v in g[f"p{i}__win"]), str(g[f"p{i}__mode"]))
+        assert np.array_equal(got.to_array(), y, equal_nan=True), i
+    r = fs.apply_activation(fs.DenseTensor3.from_array(g["relu__x"]), "relu")
+    assert np.array_equal(r.to_array().view(np.int32), g["relu__y"].view(np.int32))
+    with pytest.raises(ValueError, match="divisible"):
+        fs.pool_standalone(fs.DenseTensor3.from_array(np.ones((1, 5, 4), np.float32)), (2, 2), "max")
+
+
+def _small_vgg():
+    g = load_golden("vgg_small.npz")
+    layers = [(g[f"w{i}"], g[f"b{i}"]) for i in range(int(g["n_layers"]))]
+    net = fs.build_benchmark_net("vgg16_desk", 0.125, input_hw=32, variant=nw.VARIANT_SPARSE_FILTER)
+    weights = fs.NetworkWeights(entries=[fs.ConvParams(filters=f, bias=b) for f, b in layers])
+    return g, net, weights
+
+
+def test_vgg_stack_forward_matches_reference():
+    g, net, weights = _small_vgg()
+    prepared = fs.prepare(net, weights)
+    assert prepared.engine is not None
+    batch = [fs.DenseTensor3.from_array(a) for a in g["x"]]
+    res = fs.forward(prepared, batch)
+    got = np.stack([o.to_array() for o in res.outputs])
+    assert normwise_err(got, g["y"]) <= TOL
+    assert res.report.strategy == "strategy_i" and res.report.batch == 2
+    # per-layer path (density recording) agrees with the fused engine
+    rec = fs.forward(prepared, batch, record_density=True)
+    assert rec.report.layer_densities is not None and len(rec.report.layer_densities) == len(net.layers)
+    got2 = np.stack([o.to_array() for o in rec.outputs])
+    assert normwise_err(got2, g["y"]) <= TOL
+
+
+def test_worker_strategy_and_batch_invariance_bitwise():
+    g, net, weights = _small_vgg()
+    prepared = fs.prepare(net, weights)
+    rng = np.random.default_rng(86)
+    xs = [fs.DenseTensor3.from_array(rng.standard_normal((3, 32, 32)).astype(np.float32)) for _ in range(6)]
+    ref = [o.data.tobytes() for o in fs.forward(prepared, xs, workers=1).outputs]
+    for workers in (2, 4, 8):
+        assert [o.data.tobytes() for o in fs.forward(prepared, xs, workers=workers).outputs] == ref
+    for st in (fs.ForwardStrategy(fs.StrategyKind.STRATEGY_I), fs.ForwardStrategy(fs.StrategyKind.STRATEGY_II)):
+        assert [o.data.tobytes() for o in fs.forward(prepared, xs, strategy=st).outputs] == ref
+    # an image's result does not depend on its batch position or batch size
+    for i in (0, 3, 5):
+        assert fs.forward(prepared, [xs[i]]).outputs[0].data.tobytes() == ref[i]
+
+
+def test_forward_rejects_mismatches():
+    g, net, weights = _small_vgg()
+    p = fs.prepare(net, weights)
+    with pytest.raises(ValueError, match="nonempty"):
+        fs.forward(p, [])
+    with pytest.raises(ValueError, match="dims"):
+        fs.forward(p, [fs.DenseTensor3.from_array(np.zeros((3, 16, 16), np.float32))])
+    sp = fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.ones((3, 32, 32), np.float32)), fs.AxisOrder3.CHW)
+    with pytest.raises(ValueError, match="dense"):
+        fs.forward(p, [sp])
+
+
+def test_full_size_vgg16_config3_against_oracle(oracle):
+    """BASELINE config 3 at full size (224x224, 90% zeros): 2 images through the
+    engine vs the CPU oracle (normwise), plus the exact nnz-FLOP count."""
+    import torch
+
+    from paper_2212_08815_b200.engine import VGGEngine
+
+    layers = wl.vgg16_weights(seed=103, zero_frac=0.9)
+    x = wl.vgg16_input(2, seed=104)
+    eng = VGGEngine(layers, batch=2, hw=224)
+    y = eng.forward_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    banks = []
+    mults = 0
+    h = 224
+    for (wt, b), item in zip(layers, [it for it in wl.VGG16_PLAN if it != "M"]):
+        nodes, seg = oracle.encode_bank(wt)
+        banks.append((nodes, seg, wt.shape[0], b))
+    ref = oracle.vgg_forward(x, banks)
+    assert normwise_err(y, ref) <= TOL
+    # nnz-FLOPs per image from the engine == 2 x the oracle's exact multiply tally
+    for st, (nodes, seg, k, _) in zip(eng.steps, banks):
+        mults += oracle.sf_count(st.h, st.w, seg, len(nodes), k, 3, 3, 1, 1)
+    assert eng.flops_per_image() == 2 * mults

@@ -23,7 +23,7 @@ def main():
     hdr, units, vals = raw[0], raw[1], raw[2]
     m = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
-    scale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+    scale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
              "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
              "hz": 1.0, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
     want = {
