@@ -296,6 +296,14 @@ def main():
             cur = out
             w = w // 2 if st.pool else w
     peak_meas, peak_nom = fp32_peak_tflops(torch, _lib)
+    # DRAM traffic per launch of the dominant kernel, from the committed ncu launch list
+    # of this same command (profiles/r01_bench_launches_summary.json), when present
+    traffic, traffic_src = None, None
+    prof = os.path.join(ROOT, "profiles", "r01_bench_launches_summary.json")
+    if os.path.exists(prof) and args.workload == "c3":
+        with open(prof) as fh:
+            traffic = json.load(fh).get("sf3x3_dram_bytes_per_launch")
+        traffic_src = "profiles/r01_bench_launches_summary.json (ncu launch list, cold cache)"
     kern_ms = sum(layer_ms)
     achieved_tf = flops_img * n_local / (kern_ms * 1e-3) / 1e12
 
@@ -346,7 +354,8 @@ def main():
                          "frac_of_nominal": achieved_tf / peak_nom,
                          "hbm_gbs_peak": peaks.get("hbm_gbs"),
                          "achieved_hbm_gbs": eng.bytes_per_image() * n_local / (kern_ms * 1e-3) / 1e9,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": eng.bytes_per_image() * n_local / len(eng.steps),
                          "per_layer_ms": [round(v, 4) for v in layer_ms]},
             "gpu_launches": launches,
             "clocks": clocks,
