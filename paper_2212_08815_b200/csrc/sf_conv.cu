@@ -144,7 +144,7 @@ struct Sf3Params {
     int relu;
     int pool;                 // fused 2x2 max-pool
     int stages;               // ring depth (<= MAX_STAGES)
-    int dbg;                  // debug: 1 = walk entries without FMAs, 3 = no TMA, 4 = no bulk copies
+    int dbg;                  // debug: 1 = skip compute, 3 = no TMA, 4 = no bulk copies (1,3,4 skip compute)
 };
 
 template <int LY, bool THREADED>
@@ -245,13 +245,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     const int ly = (lane >> 2) % LY;
     const int li = lane / (4 * LY);
 
-    float acc[KT][TILE][TILE];
+    // accumulators as column pairs (FFMA2 operands): acc2[kl][py][h] = cols 2h, 2h+1
+    unsigned long long acc2[KT][TILE][2];
 #pragma unroll
     for (int a = 0; a < KT; ++a)
 #pragma unroll
-        for (int b = 0; b < TILE; ++b)
-#pragma unroll
-            for (int d = 0; d < TILE; ++d) acc[a][b][d] = 0.0f;
+        for (int b = 0; b < TILE; ++b) acc2[a][b][0] = acc2[a][b][1] = 0ull;
 
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int s = ch % STAGES;
@@ -259,34 +258,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         __syncwarp();
         const int c0 = ch * p.cc;
         const int cnt = min(p.cc, p.c - c0);
-        if (live) {
+        if (live && p.dbg == 0) {
             const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
             const int e0 = cofs[warp * (n_chunks + 1) + ch] & 1;  // offset inside aligned copy
-            uint32_t cur = smem_u32(ents + e0);
             const float *box = in_s + s * stage_in_floats + li * p.box_floats;
-            for (int cc = 0; cc < cnt; ++cc) {
-                const float *rowp = box + (cc * BOXH + TILE * ly) * BOXW + TILE * lx;
-                float pt[6][6];
-#pragma unroll
-                for (int r = 0; r < 6; ++r) {
-                    float4 a = *reinterpret_cast<const float4 *>(rowp + r * BOXW);
-                    float2 b = *reinterpret_cast<const float2 *>(rowp + r * BOXW + 4);
-                    pt[r][0] = a.x; pt[r][1] = a.y; pt[r][2] = a.z; pt[r][3] = a.w;
-                    pt[r][4] = b.x; pt[r][5] = b.y;
-                }
-                if (p.dbg >= 3) {
-                    // garbage entries: do not walk them
-                } else if (p.dbg == 0) {
-                    cur = THREADED ? sf3x3_channel_threaded(acc, pt, cur) : sf3x3_channel_looped(acc, pt, cur);
-                } else {
-                    const int2 *ep = reinterpret_cast<const int2 *>(ents) + ((cur - smem_u32(ents)) >> 3);
-                    for (;;) {
-                        const int2 en = *ep++;
-                        if (en.x < 0 || en.x >= KT * 9) break;
-                    }
-                    cur = smem_u32(ep);
-                }
-            }
+            sf3x3_chunk<BOXH * BOXW * 4>(acc2, smem_u32(ents + e0),
+                                         smem_u32(box + (TILE * ly) * BOXW + TILE * lx), cnt);
         }
         __syncwarp();
         // Stage s is free for this warp: restage its own entry run for chunk ch+STAGES;
@@ -319,7 +296,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         for (int py = 0; py < TILE; ++py)
 #pragma unroll
             for (int px = 0; px < TILE; ++px) {
-                float v = acc[kl][py][px] + b;
+                const unsigned long long pr = acc2[kl][py][px >> 1];
+                const float a = __uint_as_float((uint32_t)((px & 1) ? (pr >> 32) : (pr & 0xffffffffull)));
+                float v = a + b;
                 o[py][px] = p.relu ? relu_np(v) : v;
             }
         if (!p.pool) {
