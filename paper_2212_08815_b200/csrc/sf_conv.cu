@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 #pragma unroll
         for (int b = 0; b < TILE; ++b) acc2[a][b][0] = acc2[a][b][1] = 0ull;
 
+#pragma unroll 1
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int s = ch % STAGES;
         mbar_wait(&full[s], (ch / STAGES) & 1);

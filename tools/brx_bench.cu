@@ -6,10 +6,12 @@
 #include <cstdlib>
 #include <cstdint>
 #include "../paper_2212_08815_b200/csrc/sf3x3_dispatch.inc"
+#include "sf3x3_mask_proto.inc"
 #ifndef FSCNN_SF3_KT
 #define FSCNN_SF3_KT 4
 #endif
 
+template <int MASK>
 __global__ void __launch_bounds__(512, 1) bench(const int2 *ents_g, int n_ent, int reps, float *out, long long *cyc) {
     extern __shared__ int2 sm[];
     int2 *ents = sm;
@@ -25,7 +27,8 @@ __global__ void __launch_bounds__(512, 1) bench(const int2 *ents_g, int n_ent, i
     for (int rep = 0; rep < reps; ++rep) {
         uint32_t cur = (uint32_t)__cvta_generic_to_shared(ents);
         uint32_t end = cur + n_ent * 8;
-        while (cur < end) cur = sf3x3_chunk<34 * 20 * 4>(acc2, cur, pbase, 8);
+        if (MASK) { while (cur < end) cur = sf3x3_chunk_mask<34 * 20 * 4>(acc2, cur, pbase, 8); }
+        else { while (cur < end) cur = sf3x3_chunk<34 * 20 * 4>(acc2, cur, pbase, 8); }
     }
     long long t1 = clock64();
     float s = 0;
@@ -47,24 +50,37 @@ int main(int argc, char **argv) {
         h[k].x = FSCNN_SF3_KT * 9; h[k].y = 0; ++k;
     }
     for (int j = 0; j < 8; ++j) { h[k + j].x = FSCNN_SF3_KT * 9; h[k + j].y = 0; }
+    int mask_mode = argc > 3 ? atoi(argv[3]) : 0;
+    if (mask_mode) {
+        // per channel: m0, m1, then `per` values (distinct classes) -> 32-bit words
+        uint32_t *w = (uint32_t *)h; int q = 0; srand(1);
+        for (int c = 0; c < n_ch; ++c) {
+            unsigned long long m = 0; int got = 0;
+            while (got < per) { int j = rand() % 36; if (!(m >> j & 1)) { m |= 1ull << j; ++got; } }
+            w[q++] = (uint32_t)m; w[q++] = (uint32_t)(m >> 32);
+            for (int j = 0; j < per; ++j) { float v = 1e-3f; w[q++] = *(uint32_t *)&v; }
+        }
+        n_ent = (q + 1) / 2;  // in 8-byte units
+    }
     int2 *d; float *o; long long *cyc;
     cudaMalloc(&d, (n_ent + 8) * sizeof(int2));
     cudaMemcpy(d, h, (n_ent + 8) * sizeof(int2), cudaMemcpyHostToDevice);
     cudaMalloc(&o, 148 * 512 * 4);
     cudaMalloc(&cyc, 148 * 8);
     int smem = (n_ent + 8) * 8 + 8 * 34 * 20 * 4;
-    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto kern = mask_mode ? bench<1> : bench<0>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int warps = 4; warps <= 16; warps *= 2) {
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-        bench<<<148, 32 * warps, smem>>>(d, n_ent, 2, o, cyc);
+        kern<<<148, 32 * warps, smem>>>(d, n_ent, 2, o, cyc);
         cudaEventRecord(a);
-        bench<<<148, 32 * warps, smem>>>(d, n_ent, reps, o, cyc);
+        kern<<<148, 32 * warps, smem>>>(d, n_ent, reps, o, cyc);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         long long c0; cudaMemcpy(&c0, cyc, 8, cudaMemcpyDeviceToHost);
         double disp = (double)n_ch * per * reps;
         double fl = 148.0 * warps * 32 * disp * 32;
-        printf("per=%d fixed=%d warps/SM=%d: %.1f cycles/nonzero/warp, %.2f TFLOP/s (%s)\n", per, fixed, warps,
+        printf("mask=%d per=%d fixed=%d warps/SM=%d: %.1f cycles/nonzero/warp, %.2f TFLOP/s (%s)\n", mask_mode, per, fixed, warps,
                c0 / disp, fl / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;

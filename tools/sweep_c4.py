@@ -1,0 +1,111 @@
+"""BASELINE config 4: per-layer sparsity sweep on the 13 VGG16 conv shapes at batch 32.
+
+Sparse-filter conv (fast kernel, fused ReLU, no pool) at filter sparsity
+{50,75,90,95,99}%, and sparse-input conv (encoder on the device-resident dense input
++ the SI kernel) at input sparsity {50,75,90,95}%.  Each point: device time from
+CUDA events (median of reps), exact nnz-FLOPs, achieved TFLOP/s and fraction of the
+measured FP32 peak.  Writes JSON lines to stdout (one per point) and, with --out, a
+JSON file.
+
+usage: python tools/sweep_c4.py [--out profiles/r01_c4_sweep.json] [--layers 0,1,...] [--reps 5]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+from paper_2212_08815_b200 import device, workloads as wl
+
+
+def time_fn(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def sf_flops(wt, h, w, n):
+    """2 x exact in-bounds multiplies for 3x3/s1/p1 (kernels.py:108-133)."""
+    k, c = wt.shape[:2]
+    total = 0
+    for kh in range(3):
+        rows = sum(1 for i in range(h) if 0 <= kh + i - 1 < h)
+        for kw in range(3):
+            cols = sum(1 for j in range(w) if 0 <= kw + j - 1 < w)
+            total += int(np.count_nonzero(wt[:, :, kh, kw])) * rows * cols
+    return 2 * total * n
+
+
+def si_flops(x, k):
+    """2 x K x sum over input nonzeros of their in-bounds taps."""
+    n, c, h, w = x.shape
+    nz = x != 0
+    rows = np.array([sum(1 for kh in range(3) if 0 <= i + 1 - kh < h) for i in range(h)])
+    cols = np.array([sum(1 for kw in range(3) if 0 <= j + 1 - kw < w) for j in range(w)])
+    taps = rows[:, None] * cols[None, :]
+    return 2 * k * int((nz * taps[None, None]).sum())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--layers", default=None)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--peak", type=float, default=72.3, help="FP32 TFLOP/s denominator (measured probe)")
+    args = ap.parse_args()
+    shapes = wl.vgg16_conv_shapes()
+    layers = [int(v) for v in args.layers.split(",")] if args.layers else range(len(shapes))
+    rows = []
+    for li in layers:
+        c, k, h, w = shapes[li]
+        for zf in (0.5, 0.75, 0.9, 0.95, 0.99):
+            x, wt, b = wl.sweep_layer(li, "sf", zf, n=args.n)
+            bank = device.sf_pack(torch.from_numpy(wt).cuda())
+            xh = device.to_halo(torch.from_numpy(x).cuda())
+            bias = torch.from_numpy(b).cuda()
+            out = device.halo_empty(args.n, k, h, w)
+            ms = time_fn(lambda: device.sf_conv3x3(xh, bank, bias, True, False, out=out, w=w), args.reps)
+            fl = sf_flops(wt, h, w, args.n)
+            r = {"mode": "sf", "layer": li, "shape": [c, k, h, w], "zero_frac": zf, "ms": ms,
+                 "nnz_gflop": fl / 1e9, "tflops": fl / (ms * 1e-3) / 1e12}
+            r["frac_of_fp32_peak"] = r["tflops"] / args.peak
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del xh, out, bank
+        for zf in (0.5, 0.75, 0.9, 0.95):
+            x, wt, b = wl.sweep_layer(li, "si", zf, n=args.n)
+            xd = torch.from_numpy(x).cuda()
+            wcrsk = device.kcrs_to_crsk(torch.from_numpy(wt).cuda())
+            enc = device.encode_order(xd, "CHW")
+            out = torch.empty((args.n, k, h, w), dtype=torch.float32, device="cuda")
+            ms = time_fn(lambda: device.si_conv(enc.nodes, enc.seg_off, args.n, c, h, w, wcrsk, k, 3, 3, 1, 1,
+                                                out=out), args.reps)
+            fl = si_flops(x, k)
+            r = {"mode": "si", "layer": li, "shape": [c, k, h, w], "zero_frac": zf, "ms": ms,
+                 "nnz_gflop": fl / 1e9, "tflops": fl / (ms * 1e-3) / 1e12}
+            r["frac_of_fp32_peak"] = r["tflops"] / args.peak
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del xd, enc, out
+        torch.cuda.empty_cache()
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump(rows, fh, indent=0)
+
+
+if __name__ == "__main__":
+    main()
