@@ -107,31 +107,34 @@ int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_
  * accumulation order).  Consumes the kernel-side packed filter stream:
  *   the filter bank regrouped into groups of `kt` filters; for group g and input
  *   channel c, segment g*c_n + c lists the nonzeros W[g*kt + kl][c][kh][kw] as
- *   nodes with index = kl*9 + kh*3 + kw, ascending, terminated by a sentinel whose
- *   index is kt*9 (the kernel jump table's exit target) rather than -1.
+ *   nodes with index = kl*9 + kh*3 + kw, ascending, then a sentinel slot.  The last
+ *   nonzero of a segment carries index + kt*9 (its jump-table variant that falls into
+ *   the channel transition) and an empty segment's sentinel slot carries 2*kt*9
+ *   (transition without arithmetic); other sentinel slots are never dispatched.
  * Build it with fscnn_sf_pack_offsets / fscnn_sf_pack_nodes from a dense
  * [K][C][3][3] bank (itself decoded from the reference's CHW SparseTensor4 by
  * fscnn_decode, or straight from dense weights).
  * ------------------------------------------------------------------------- */
-int fscnn_sf_pack_kt(void); /* filters per group the fast kernel expects */
-int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int64_t *seg_off,
+int fscnn_sf_pack_kt(void); /* default filters per group (the kernel supports kt = 4 and 8) */
+int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *seg_off,
                           int64_t *total_nodes, void *workspace, size_t workspace_bytes,
                           void *stream);
-int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, const int64_t *seg_off,
-                        fscnn_node *nodes, void *stream);
+int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, int kt, const int64_t *seg_off,
+                        int64_t total_nodes, fscnn_node *nodes, void *stream);
 /* Fast conv.  x: [n][c][h][ldi] (ldi >= w, ldi % 4 == 0, 16-byte aligned; the
  * columns w..ldi-1 are never read).  y: [n][k][h][ldo], or with pool != 0 the fused
  * 2x2 max-pool result [n][k][h/2][ldo].  packed/packed_seg_off/total_nodes: the
  * packed stream (allocate total_nodes + 2 nodes: the kernel bulk-copies 16-byte
  * aligned ranges).  max_chunk_entries: the largest node count (sentinels included)
  * of any group over any run of `cc` consecutive channels.  ly selects the
- * sub-region height 4*ly (8, 4 or 2; 0 = by h).  relu applies np.maximum(.,0)
- * before the pool, as the reference's conv -> relu -> pool sequence does. */
+ * sub-region height 4*ly (8, 4 or 2; 0 = by h).  kt: the stream's filters per group
+ * (4 or 8).  relu applies np.maximum(.,0) before the pool, as the reference's
+ * conv -> relu -> pool sequence does. */
 int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
                         const fscnn_node *packed, const int64_t *packed_seg_off,
                         int64_t total_nodes, int max_chunk_entries, int cc, int k,
                         const float *bias, int relu, int pool, float *y, int ldo, int ly,
-                        void *stream);
+                        int kt, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Sparse-Input convolution (bit-exact).
@@ -148,6 +151,14 @@ int fscnn_si_conv(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, 
                   const float *bias, float *y, void *stream);
 int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w_crsk,
                        void *stream);
+/* 3x3 / stride 1 / pad 1 fast path, same bit-exact results: a warp owns 32 filters and a
+ * strip of 8 outputs of one row and walks the strip's input columns left to right (the
+ * reference's kw-outer order per output), applying each node to up to three outputs with
+ * one 16-byte weight load.  wq: [c][kh][K] float4 {w(kw=0), w(kw=1), w(kw=2), 0} built
+ * by fscnn_si_pack3x3 from a dense [K][C][3][3] bank (c*3*K float4 = 48*c*K bytes). */
+int fscnn_si_pack3x3(const float *w_kc33, int k, int c, float *wq, void *stream);
+int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
+                     int w, const float *wq, int k, const float *bias, float *y, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Dense layers between convolutions.

@@ -35,11 +35,13 @@ _SIGNATURES = {
     "fscnn_decode": (_i32, [_vp, _vp] + [_i64] * 4 + [_vp] + [_i64] * 4 + [_vp]),
     "fscnn_sf_conv_exact": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "fscnn_sf_pack_kt": (_i32, []),
-    "fscnn_sf_pack_offsets": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
-    "fscnn_sf_pack_nodes": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
-    "fscnn_sf_conv3x3_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp]),
+    "fscnn_sf_pack_offsets": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "fscnn_sf_pack_nodes": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
+    "fscnn_sf_conv3x3_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _i32, _vp]),
     "fscnn_si_conv": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fscnn_kcrs_to_crsk": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fscnn_si_pack3x3": (_i32, [_vp, _i32, _i32, _vp, _vp]),
+    "fscnn_si_conv3x3": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
     "fscnn_relu": (_i32, [_vp, _i64, _vp, _vp]),
     "fscnn_pool2d": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_whc_to_nchw": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),

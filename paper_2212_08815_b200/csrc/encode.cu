@@ -277,7 +277,21 @@ __global__ void decode_kernel(const int2 *nodes, const int64_t *seg_off, int64_t
     }
 }
 
-constexpr int kSfPackKt = 4;  // must match KT (FSCNN_SF3_KT) in sf_conv.cu
+constexpr int kSfPackKt = 4;  // default filters per group (sf_conv.cu supports 4 and 8)
+
+// Fast-stream marking: the last nonzero of every (group, channel) segment gets
+// index + kt*9 (its jump-table variant that falls into the channel transition);
+// an empty segment's sentinel slot becomes index 2*kt*9 (transition without FMAs).
+// Other sentinel slots are skipped by the kernel and never dispatched.
+__global__ void sf_pack_mark_kernel(int2 *nodes, const int64_t *seg_off, int64_t n_seg,
+                                    int64_t total, int classes) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    int64_t start = seg_off[s];
+    int64_t end = (s + 1 < n_seg) ? seg_off[s + 1] : total;  // one past the sentinel
+    if (end - start == 1) nodes[start].x = 2 * classes;
+    else nodes[end - 2].x += classes;
+}
 
 }  // namespace
 
@@ -340,23 +354,30 @@ int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
 
 int fscnn_sf_pack_kt(void) { return kSfPackKt; }
 
-int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int64_t *seg_off,
+int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *seg_off,
                           int64_t *total_nodes, void *workspace, size_t workspace_bytes,
                           void *stream) {
     FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && total_nodes, "bad pack arguments");
-    int64_t groups = ceil_div(k, kSfPackKt);
-    SfPackSrc src{w_kc33, k, c, kSfPackKt, kSfPackKt * 9};
+    FSCNN_REQUIRE(kt == 4 || kt == 8, "kt must be 4 or 8");
+    int64_t groups = ceil_div(k, kt);
+    SfPackSrc src{w_kc33, k, c, kt, (int64_t)kt * 9};
     return encode_offsets_impl(src, groups * c, false, seg_off, total_nodes, workspace,
                                workspace_bytes, as_stream(stream));
 }
 
-int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, const int64_t *seg_off,
-                        fscnn_node *nodes, void *stream) {
+int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, int kt, const int64_t *seg_off,
+                        int64_t total_nodes, fscnn_node *nodes, void *stream) {
     FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && nodes, "bad pack arguments");
-    int64_t groups = ceil_div(k, kSfPackKt);
-    SfPackSrc src{w_kc33, k, c, kSfPackKt, kSfPackKt * 9};
-    // the fast kernel's jump table maps index kt*9 to its loop exit: that is the sentinel
-    return encode_nodes_impl(src, groups * c, false, seg_off, nodes, as_stream(stream), kSfPackKt * 9);
+    FSCNN_REQUIRE(kt == 4 || kt == 8, "kt must be 4 or 8");
+    int64_t groups = ceil_div(k, kt);
+    SfPackSrc src{w_kc33, k, c, kt, (int64_t)kt * 9};
+    cudaStream_t st = as_stream(stream);
+    int rc = encode_nodes_impl(src, groups * c, false, seg_off, nodes, st, kt * 9);
+    if (rc != FSCNN_OK) return rc;
+    sf_pack_mark_kernel<<<(unsigned)ceil_div(groups * c, 256), 256, 0, st>>>(
+        reinterpret_cast<int2 *>(nodes), seg_off, groups * c, total_nodes, kt * 9);
+    FSCNN_LAUNCH_CHECK("sf_pack_mark_kernel");
+    return FSCNN_OK;
 }
 
 }  // extern "C"

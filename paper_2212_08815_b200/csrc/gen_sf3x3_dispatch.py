@@ -3,11 +3,13 @@ kernel for one staged chunk of input channels, as one inline-PTX block with a re
 jump table.
 
 Per chunk the lane walks a warp-uniform entry list: for each channel, the entries
-(index = kl*9 + kh*3 + kw, value) of its filter group, then the channel sentinel
-(index KT*9).  A jump table (`brx.idx`) sends each entry to code that applies it to
-the lane's 4x4 output tile of filter kl with statically named registers, and sends
-the sentinel to the channel transition (advance the patch pointer, reload the 6x6
-input patch from shared memory, stop after the chunk's last channel).  Why PTX: a
+(index = kl*9 + kh*3 + kw, value) of its filter group and a sentinel slot.  A jump
+table (`brx.idx`) sends each entry to code that applies it to the lane's 4x4 output
+tile of filter kl with statically named registers.  The channel's last entry carries
+index + KT*9: its variant applies the entry and falls straight into the channel
+transition (skip the sentinel slot, advance the patch pointer, reload the 6x6 input
+patch, stop after the chunk's last channel) -- no extra dispatch per channel.  An
+empty channel's sentinel slot carries 2*KT*9 (transition only).  Why PTX: a
 C++ switch becomes a 6-level compare tree and spills; this is one indirect branch per
 nonzero and no per-channel call overhead.
 
@@ -17,18 +19,16 @@ Arithmetic: accumulators and the patch are held as 64-bit register pairs
 issue slots); kw = 1 straddles the pairs and runs as 16 scalar FFMA on the halves.
 The next entry is prefetched one step ahead.
 
-Operands (all via the C++ wrapper sf3x3_chunk below):
-  %0..%31   acc pairs  acc2[kl][py][h]  (kl*8 + py*2 + h), h=0: cols 0,1  h=1: cols 2,3
-  %32..%49  patch pairs pt2[r][h]        (r*3 + h),         h: cols 2h, 2h+1
-  %50       entry cursor (shared address; on exit: past the chunk's last sentinel)
-  %51       patch cursor (shared address of the current channel's patch, row 0 col 0)
-  %52       channels left in the chunk (>= 1)
-  %53       channel pitch of a staged box in bytes (immediate; row pitch is 80 B)
+Operands (all via the C++ wrapper sf3x3_chunk below; NA = 8*KT):
+  %0..%NA-1     acc pairs  acc2[kl][py][h]  (kl*8 + py*2 + h), h=0: cols 0,1  h=1: cols 2,3
+  next 18       patch pairs pt2[r][h]        (r*3 + h),         h: cols 2h, 2h+1
+  then          entry cursor, patch cursor (shared addresses), channels left in the chunk,
+                channel pitch of a staged box in bytes (immediate; row pitch is 80 B)
 
 Run: python gen_sf3x3_dispatch.py > sf3x3_dispatch.inc
 """
 
-KT, TILE, PATCH = 4, 4, 6
+TILE, PATCH = 4, 6
 
 
 ROW_BYTES = 80  # smem row pitch of a staged box: 20 floats (BOXW in sf_conv.cu)
@@ -40,18 +40,21 @@ def load_patch(e, P, PP):
         e(f"ld.shared.b64 {P(r, 2)}, [{PP}+{r * ROW_BYTES + 16}];")
 
 
-def block() -> str:
+def block(KT: int) -> str:
+    NA = KT * 8                                              # acc pair operands
     A = lambda kl, py, h: f"%{kl * 8 + py * 2 + h}"          # acc pair
-    P = lambda r, h: f"%{32 + r * 3 + h}"                    # patch pair
-    CUR, PP, CNT, CHS = "%50", "%51", "%52", "%53"
+    P = lambda r, h: f"%{NA + r * 3 + h}"                    # patch pair
+    CUR, PP, CNT, CHS = (f"%{NA + 18 + i}" for i in range(4))
+    NC = KT * 9
     L = []
     e = L.append
     e("{")
     e(".reg .pred p_end;")
-    e(".reg .b32 r_ix, r_i1, r_v1, r_t, r_a, r_b, r_c, r_d, r_e, r_f;")
+    e(".reg .b32 r_ix, r_i1, r_v1, r_a, r_b, r_c, r_d, r_e, r_f;")
     e(".reg .f32 f_v;")
     e(".reg .b64 d_vv;")
-    targets = ", ".join([f"C{i}_%=" for i in range(KT * 9)] + ["S_%="])
+    # targets: 0..NC-1 entry, NC..2NC-1 channel-last entry, 2NC empty channel
+    targets = ", ".join([f"C{i}_%=" for i in range(NC)] + [f"X{i}_%=" for i in range(NC)] + ["E_%="])
     e(f"T_%=: .branchtargets {targets};")
     load_patch(e, P, PP)
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
@@ -63,34 +66,53 @@ def block() -> str:
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
     e(f"add.u32 {CUR}, {CUR}, 8;")
     e("brx.idx.uni r_ix, T_%=;")
+
+    def fmas(kl, tap):
+        kh, kw = divmod(tap, 3)
+        for py in range(TILE):
+            r = py + kh
+            if kw in (0, 2):
+                for h in range(2):
+                    src = P(r, h + kw // 2)
+                    a = A(kl, py, h)
+                    e(f"fma.rn.f32x2 {a}, d_vv, {src}, {a};")
+            else:
+                # window cols 1..4 = hi(pair0), lo(pair1), hi(pair1), lo(pair2)
+                e(f"mov.b64 {{r_a, r_b}}, {P(r, 0)};")
+                e(f"mov.b64 {{r_c, r_d}}, {P(r, 1)};")
+                e(f"mov.b64 {{r_e, r_f}}, {P(r, 2)};")
+                for h in range(2):
+                    lo_src, hi_src = (("r_b", "r_c"), ("r_d", "r_e"))[h]
+                    a = A(kl, py, h)
+                    e("{ .reg .f32 x, y;")
+                    e(f"mov.b64 {{x, y}}, {a};")
+                    e(f"fma.rn.f32 x, f_v, {lo_src}, x;")
+                    e(f"fma.rn.f32 y, f_v, {hi_src}, y;")
+                    e(f"mov.b64 {a}, {{x, y}};")
+                    e("}")
+
     for kl in range(KT):
         for tap in range(9):
-            kh, kw = divmod(tap, 3)
             e(f"C{kl * 9 + tap}_%=:")
-            for py in range(TILE):
-                r = py + kh
-                if kw in (0, 2):
-                    for h in range(2):
-                        src = P(r, h + kw // 2)
-                        a = A(kl, py, h)
-                        e(f"fma.rn.f32x2 {a}, d_vv, {src}, {a};")
-                else:
-                    # window cols 1..4 = hi(pair0), lo(pair1), hi(pair1), lo(pair2)
-                    e(f"mov.b64 {{r_a, r_b}}, {P(r, 0)};")
-                    e(f"mov.b64 {{r_c, r_d}}, {P(r, 1)};")
-                    e(f"mov.b64 {{r_e, r_f}}, {P(r, 2)};")
-                    for h in range(2):
-                        lo_src, hi_src = (("r_b", "r_c"), ("r_d", "r_e"))[h]
-                        a = A(kl, py, h)
-                        e("{ .reg .f32 x, y;")
-                        e(f"mov.b64 {{x, y}}, {a};")
-                        e(f"fma.rn.f32 x, f_v, {lo_src}, x;")
-                        e(f"fma.rn.f32 y, f_v, {hi_src}, y;")
-                        e(f"mov.b64 {a}, {{x, y}};")
-                        e("}")
+            fmas(kl, tap)
             e("bra.uni N_%=;")
-    # channel sentinel: next channel or done
+    for kl in range(KT):
+        for tap in range(9):
+            e(f"X{kl * 9 + tap}_%=:")
+            fmas(kl, tap)
+            e("bra.uni S_%=;")
+    # channel-last entry: the prefetched slot was the segment's sentinel; skip it
     e("S_%=:")
+    e(f"sub.u32 {CNT}, {CNT}, 1;")
+    e(f"setp.eq.u32 p_end, {CNT}, 0;")
+    e("@p_end bra.uni D_%=;")
+    e(f"add.u32 {PP}, {PP}, {CHS};")
+    load_patch(e, P, PP)
+    e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
+    e(f"add.u32 {CUR}, {CUR}, 8;")
+    e("bra.uni N_%=;")
+    # empty channel: the prefetched entry already belongs to the next channel
+    e("E_%=:")
     e(f"sub.u32 {CNT}, {CNT}, 1;")
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
     e("@p_end bra.uni D_%=;")
@@ -98,32 +120,33 @@ def block() -> str:
     load_patch(e, P, PP)
     e("bra.uni N_%=;")
     e("D_%=:")
-    # the entry after the last sentinel was prefetched: step back over it
-    e(f"sub.u32 {CUR}, {CUR}, 8;")
     e("}")
     return "\\n\\t".join(L)
 
 
-def main():
-    print("// GENERATED by gen_sf3x3_dispatch.py -- do not edit by hand.")
-    print("// One staged chunk of input channels of the fast sparse-filter kernel: walk the")
-    print("// warp-uniform entry list (index = kl*9 + kh*3 + kw, value; channel sentinel")
-    print(f"// index {KT * 9}) and apply each nonzero to the lane's 4x4 output tile of filter kl.")
-    print(f"#define FSCNN_SF3_KT {KT}")
+def emit(KT: int) -> None:
     outs = ", ".join(f'"+l"(acc2[{kl}][{py}][{h}])' for kl in range(KT) for py in range(TILE) for h in range(2))
     pts = ", ".join(f'"=l"(pt2[{r}][{h}])' for r in range(PATCH) for h in range(3))
     print("template <int CH_BYTES>")
-    print(f"__device__ __forceinline__ uint32_t sf3x3_chunk(unsigned long long (&acc2)[{KT}][4][2],")
-    print("                                           uint32_t cur, uint32_t patch, uint32_t n_ch) {")
+    print(f"__device__ __forceinline__ void sf3x3_chunk(unsigned long long (&acc2)[{KT}][4][2],")
+    print("                                            uint32_t cur, uint32_t patch, uint32_t n_ch) {")
     print("    unsigned long long pt2[6][3];")
-    print(f'    asm volatile("{block()}"')
+    print(f'    asm volatile("{block(KT)}"')
     print(f"                 : {outs},")
     print(f"                   {pts},")
     print('                   "+r"(cur), "+r"(patch), "+r"(n_ch)')
     print('                 : "n"(CH_BYTES)')
     print('                 : "memory");')
-    print("    return cur;")
     print("}")
+    print()
+
+
+def main():
+    print("// GENERATED by gen_sf3x3_dispatch.py -- do not edit by hand.")
+    print("// One staged chunk of input channels of the fast sparse-filter kernel (overloads")
+    print("// for KT = 4 and 8 filters per warp); see the generator for the protocol.")
+    for kt in (4, 8):
+        emit(kt)
 
 
 if __name__ == "__main__":

@@ -70,9 +70,13 @@ __global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, i
 // ------------------------------------------------------------------------------
 // fast 3x3 kernel
 // ------------------------------------------------------------------------------
-constexpr int KT = FSCNN_SF3_KT;   // filters per warp group (== fscnn_sf_pack_kt)
-constexpr int NWARP = 8;           // warps per CTA -> 32 filters per CTA; 2 CTAs per SM
-constexpr int NTHREADS = NWARP * 32;         // warp 0 lane 0 doubles as the TMA producer
+// KT filters per warp (4 or 8, == the pack's kt); a CTA always holds 32 filters:
+// KT=4 -> 8 warps (<=128 regs, 2 CTAs = 16 warps/SM), KT=8 -> 4 warps (2 CTAs = 8 warps/SM)
+constexpr int CTA_FILTERS = 32;
+template <int KT> struct SfCfg {
+    static constexpr int NWARP = CTA_FILTERS / KT;
+    static constexpr int NTHREADS = NWARP * 32;
+};
 constexpr int MAX_STAGES = 4;
 constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
 constexpr int TILE = 4;            // lane tile is TILE x TILE outputs
@@ -147,9 +151,11 @@ struct Sf3Params {
     int dbg;                  // debug: 1 = skip compute, 3 = no TMA, 4 = no bulk copies (1,3,4 skip compute)
 };
 
-template <int LY, bool THREADED>
-__global__ void __launch_bounds__(NTHREADS, 2)
+template <int LY, int KT>
+__global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, 2)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
+    constexpr int NWARP = SfCfg<KT>::NWARP;
+    constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
     constexpr int LI = 8 / LY;          // sub-regions per CTA
     constexpr int SUBH = TILE * LY;     // sub-region height
     constexpr int BOXH = SUBH + 2;
@@ -361,7 +367,7 @@ EncodeTiledFn get_encode_tiled() {
     return fn;
 }
 
-template <int LY, bool THREADED>
+template <int LY, int KT>
 int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     constexpr int LI = 8 / LY;
     constexpr int SUBH = TILE * LY;
@@ -371,6 +377,8 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     p.box_floats = BOXW * (SUBH + 2) * p.cc;
     // each box must start 128-byte aligned (TMA destination)
     p.box_floats = (p.box_floats + 31) & ~31;
+    constexpr int NWARP = SfCfg<KT>::NWARP;
+    constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
     const int n_chunks = (int)ceil_div(p.c, p.cc);
     auto smem_for = [&](int st) {
         return (size_t)st * LI * p.box_floats * 4 + (size_t)st * NWARP * p.ent_cap * 8 + 2 * st * 8 +
@@ -384,7 +392,7 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
         return FSCNN_ERR_UNSUPPORTED;
     }
-    auto kern = sf3x3_kernel<LY, THREADED>;
+    auto kern = sf3x3_kernel<LY, KT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("sf3x3: smem attribute (%zu bytes): %s", smem, cudaGetErrorString(e));
@@ -428,7 +436,7 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
                         const fscnn_node *packed, const int64_t *packed_seg_off,
                         int64_t total_nodes, int max_chunk_entries, int cc, int k,
                         const float *bias, int relu, int pool, float *y, int ldo, int ly,
-                        void *stream) {
+                        int kt, void *stream) {
     static const int dbg_mode = getenv("FSCNN_SF3_DEBUG") ? atoi(getenv("FSCNN_SF3_DEBUG")) : 0;
     FSCNN_REQUIRE(n > 0 && c > 0 && h > 0 && w > 0 && k > 0, "bad extents");
     FSCNN_REQUIRE(ldi >= w + 1 && ldi % 4 == 0, "input row pitch must be >= w + 1 and a multiple of 4");
@@ -470,15 +478,14 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
         return FSCNN_ERR_CUDA;
     }
     cudaStream_t st = as_stream(stream);
-    static const int threaded = getenv("FSCNN_SF3_THREADED") ? atoi(getenv("FSCNN_SF3_THREADED")) : 0;
-    switch (ly * 2 + (threaded ? 1 : 0)) {
-        case 17: return launch_sf3x3<8, true>(map, p, st);
-        case 9: return launch_sf3x3<4, true>(map, p, st);
-        case 5: return launch_sf3x3<2, true>(map, p, st);
-        case 16: return launch_sf3x3<8, false>(map, p, st);
-        case 8: return launch_sf3x3<4, false>(map, p, st);
-        case 4: return launch_sf3x3<2, false>(map, p, st);
-        default: set_error("unsupported sub-region height %d", ly); return FSCNN_ERR_ARG;
+    switch (ly * 16 + kt) {
+        case 8 * 16 + 4: return launch_sf3x3<8, 4>(map, p, st);
+        case 4 * 16 + 4: return launch_sf3x3<4, 4>(map, p, st);
+        case 2 * 16 + 4: return launch_sf3x3<2, 4>(map, p, st);
+        case 8 * 16 + 8: return launch_sf3x3<8, 8>(map, p, st);
+        case 4 * 16 + 8: return launch_sf3x3<4, 8>(map, p, st);
+        case 2 * 16 + 8: return launch_sf3x3<2, 8>(map, p, st);
+        default: set_error("unsupported sub-region height %d / kt %d", ly, kt); return FSCNN_ERR_ARG;
     }
 }
 

@@ -9,6 +9,8 @@
 // transposed [c][kh][kw][K] bank are one coalesced 128-byte line per node.
 // Results equal to zero are written as +0.0 (the reference stores no node and
 // densify yields +0.0), then + bias[k] when a bias is given (layers.py:425-428).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fscnn {
@@ -51,12 +53,110 @@ __global__ void __launch_bounds__(kPixPerBlock * 32)
     y[(((int64_t)img * k_n + k) * n_h + i) * n_w + j] = v;
 }
 
+// 3x3 / stride 1 / pad 1 strip kernel (every VGG16 shape).  A warp owns 32 filters
+// (lane = k) and a strip of S consecutive outputs (i, j0..j0+S-1).  It walks the
+// strip's input columns w_in = j0-1 .. j0+S left to right and, within a column, rows
+// h_in = i-1 .. i+1, then the column's channel fiber.  For output j' the tap of
+// column w_in is l = w_in - j' + 1, so each output sees its contributions with l
+// ascending (outer), kh ascending, c ascending -- the reference order -- and the
+// sums are bit-identical.  Each node loads its three kw weights for this lane with
+// one 16-byte load from the [c][kh][K][4] bank and updates up to three outputs.
+template <int S>
+__global__ void __launch_bounds__(128, 8)
+    si_strip_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int c_n,
+                    int h_i, int w_i, const float4 *__restrict__ wq, int k_n, int strips,
+                    const float *__restrict__ bias, float *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int job = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (job >= h_i * strips) return;
+    const int i = job / strips, j0 = (job % strips) * S;
+    const int k = blockIdx.y * 32 + lane;
+    const int img = blockIdx.z;
+    const bool live = k < k_n;
+    const int kq = live ? k : 0;
+    const int64_t *so = seg_off + (int64_t)img * h_i * w_i;
+    float acc[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) acc[t] = 0.0f;
+#pragma unroll
+    for (int col = 0; col < S + 2; ++col) {
+        const int w_in = j0 - 1 + col;
+        if (w_in < 0 || w_in >= w_i) continue;
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+            const int h_in = i - 1 + kk;
+            if (h_in < 0 || h_in >= h_i) continue;
+            int64_t q = so[(int64_t)w_in * h_i + h_in];
+            for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) {
+                const float v = __int_as_float(nd.y);
+                const float4 wv = wq[((int64_t)nd.x * 3 + kk) * k_n + kq];
+                // output j' = col - l (strip-relative), tap l = 0,1,2
+#pragma unroll
+                for (int l = 0; l < 3; ++l) {
+                    const int jp = col - l;
+                    if (jp < 0 || jp >= S) continue;
+                    const float w = l == 0 ? wv.x : (l == 1 ? wv.y : wv.z);
+                    acc[jp] = __fadd_rn(acc[jp], __fmul_rn(w, v));
+                }
+            }
+        }
+    }
+    if (!live) return;
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        const int j = j0 + t;
+        if (j >= w_i) break;
+        float v = (acc[t] != 0.0f) ? acc[t] : 0.0f;
+        if (bias) v = __fadd_rn(v, bias[k]);
+        y[(((int64_t)img * k_n + k) * h_i + i) * w_i + j] = v;
+    }
+}
+
+__global__ void kcrs_to_ckq_kernel(const float *__restrict__ w, int k_n, int c_n,
+                                   float4 *__restrict__ out) {
+    int64_t total = (int64_t)c_n * 3 * k_n;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        int k = (int)(t % k_n);
+        int64_t r = t / k_n;
+        int kh = (int)(r % 3);
+        int c = (int)(r / 3);
+        const float *src = w + (((int64_t)k * c_n + c) * 3 + kh) * 3;  // [K][C][3][3] row kh
+        out[t] = make_float4(src[0], src[1], src[2], 0.0f);
+    }
+}
+
 }  // namespace
 }  // namespace fscnn
 
 using namespace fscnn;
 
 extern "C" {
+
+int fscnn_si_pack3x3(const float *w_kc33, int k, int c, float *wq, void *stream) {
+    FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && wq, "bad SI pack arguments");
+    int64_t total = (int64_t)c * 3 * k;
+    unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    kcrs_to_ckq_kernel<<<blocks, 256, 0, as_stream(stream)>>>(w_kc33, k, c,
+                                                              reinterpret_cast<float4 *>(wq));
+    FSCNN_LAUNCH_CHECK("kcrs_to_ckq_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
+                     int w, const float *wq, int k, const float *bias, float *y, void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
+    if (n == 0 || k == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(in_nodes && in_seg_off && wq && y, "null buffer");
+    constexpr int S = 8;
+    const int strips = (int)ceil_div(w, S);
+    dim3 grid((unsigned)ceil_div((int64_t)h * strips, 4), (unsigned)ceil_div(k, 32), (unsigned)n);
+    si_strip_kernel<S><<<grid, 128, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2 *>(in_nodes), in_seg_off, c, h, w,
+        reinterpret_cast<const float4 *>(wq), k, strips, bias, y);
+    FSCNN_LAUNCH_CHECK("si_strip_kernel");
+    return FSCNN_OK;
+}
 
 int fscnn_si_conv(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
                   int w, const float *wt, int k, int h_f, int w_f, int stride, int pad,

@@ -136,7 +136,8 @@ def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None
 
 # -- sparse-filter conv ------------------------------------------------------------------
 
-STAGES, NWARP, BOXW, SUBW, TILE = 2, 8, 20, 16, 4  # STAGES: the minimum ring the kernel runs with
+STAGES, BOXW, SUBW, TILE = 2, 20, 16, 4  # STAGES: the minimum ring the kernel runs with
+CTA_FILTERS = 32  # filters per CTA: 32 // kt warps
 SMEM_LIMIT = 227 * 1024
 
 
@@ -144,7 +145,8 @@ def _align(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int) -> int:
+def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4) -> int:
+    NWARP = CTA_FILTERS // kt
     li = 8 // ly
     box = _align(BOXW * (TILE * ly + 2) * cc, 32)
     n_chunks = math.ceil(c / cc)
@@ -169,6 +171,7 @@ class PackedBank:
 
     k: int
     c: int
+    kt: int                    # filters per group (4 or 8)
     nodes: torch.Tensor        # int32 [total + 2, 2]
     seg_off: torch.Tensor      # int64 [groups * c]
     total: int
@@ -193,18 +196,27 @@ class PackedBank:
             cnt = np.pad(self.counts, ((0, 0), (0, pad)))
             mx = int(cnt.reshape(cnt.shape[0], n_chunks, cc).sum(axis=2).max())
             ent_cap = (mx + 4) & ~1
-            if sf3x3_smem_bytes(ly, cc, ent_cap, self.c) <= SMEM_LIMIT:
+            if sf3x3_smem_bytes(ly, cc, ent_cap, self.c, self.kt) <= SMEM_LIMIT:
                 self._cache[ly] = (cc, mx)
                 return cc, mx
         raise RuntimeError("filter bank too dense for the fast kernel's shared memory")
 
 
-def sf_pack(w_kc33: torch.Tensor) -> PackedBank:
+def default_kt(c: int) -> int:
+    """Filters per warp group: 8 halves the per-channel patch reloads (shared-memory
+    bound at 4) at half the resident warps; the env var FSCNN_SF3_KT overrides."""
+    import os
+
+    forced = int(os.environ.get("FSCNN_SF3_KT", "0"))
+    return forced if forced in (4, 8) else int(_lib.load().fscnn_sf_pack_kt())
+
+
+def sf_pack(w_kc33: torch.Tensor, kt: int | None = None) -> PackedBank:
     """Pack a dense [K, C, 3, 3] bank (device) into the fast kernel's stream."""
     assert w_kc33.dim() == 4 and tuple(w_kc33.shape[2:]) == (3, 3)
     w = w_kc33.contiguous()
     k, c = int(w.shape[0]), int(w.shape[1])
-    kt = int(_lib.load().fscnn_sf_pack_kt())
+    kt = int(kt or default_kt(c))
     groups = math.ceil(k / kt)
     dev = _dev()
     seg = torch.empty(groups * c, dtype=torch.int64, device=dev)
@@ -212,15 +224,15 @@ def sf_pack(w_kc33: torch.Tensor) -> PackedBank:
     ws_bytes = int(_lib.load().fscnn_encode_workspace_bytes(groups * c))
     ws = torch.empty(ws_bytes // 8 + 1, dtype=torch.int64, device=dev)
     st = stream()
-    call("fscnn_sf_pack_offsets", ptr(w), k, c, ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
+    call("fscnn_sf_pack_offsets", ptr(w), k, c, kt, ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
     n = int(total.item())
     nodes = torch.empty((n + 2, 2), dtype=torch.int32, device=dev)
     nodes[n:].fill_(-1)
-    call("fscnn_sf_pack_nodes", ptr(w), k, c, ptr(seg), ptr(nodes), st)
+    call("fscnn_sf_pack_nodes", ptr(w), k, c, kt, ptr(seg), n, ptr(nodes), st)
     so = seg.cpu().numpy()
     ends = np.append(so[1:], n)
     counts = (ends - so).reshape(groups, c)
-    return PackedBank(k, c, nodes, seg, n, counts, int(n - groups * c))
+    return PackedBank(k, c, kt, nodes, seg, n, counts, int(n - groups * c))
 
 
 def halo_pitch(w: int) -> int:
@@ -269,7 +281,7 @@ def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, rel
         out = halo_empty(n, bank.k, ho, wo, x.device)
     ldo = int(out.stride(2))
     call("fscnn_sf_conv3x3_ex", ptr(x), n, c, h, w, ldi, ptr(bank.nodes), ptr(bank.seg_off),
-         bank.total, mx, cc, bank.k, ptr(bias), int(relu), int(pool), ptr(out), ldo, ly, stream())
+         bank.total, mx, cc, bank.k, ptr(bias), int(relu), int(pool), ptr(out), ldo, ly, bank.kt, stream())
     return out
 
 
@@ -309,6 +321,25 @@ def si_conv(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, 
         out = torch.empty((n, k, n_h, n_w), dtype=torch.float32, device=nodes.device)
     call("fscnn_si_conv", ptr(nodes), ptr(seg_off), n, c, h, w, ptr(wt_crsk), k, h_f, w_f,
          stride_, pad, ptr(bias), ptr(out), stream())
+    return out
+
+
+def si_pack3x3(w_kc33: torch.Tensor) -> torch.Tensor:
+    """Dense [K, C, 3, 3] bank -> the strip kernel's [C][3][K] float4 layout."""
+    w = w_kc33.contiguous()
+    k, c = int(w.shape[0]), int(w.shape[1])
+    out = torch.empty((c, 3, k, 4), dtype=torch.float32, device=w.device)
+    call("fscnn_si_pack3x3", ptr(w), k, c, ptr(out), stream())
+    return out
+
+
+def si_conv3x3(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,
+               wq: torch.Tensor, k: int, bias: torch.Tensor | None = None,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """3x3/s1/p1 sparse-input conv (strip kernel), bit-exact with kernels.py:136-166."""
+    if out is None:
+        out = torch.empty((n, k, h, w), dtype=torch.float32, device=nodes.device)
+    call("fscnn_si_conv3x3", ptr(nodes), ptr(seg_off), n, c, h, w, ptr(wq), k, ptr(bias), ptr(out), stream())
     return out
 
 

@@ -172,8 +172,11 @@ def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, pad
     nodes, seg = kernels.sparse_to_device(t_in)
     c, h, w = t_in.dims
     _, h_f, w_f = filters[0].dims
-    wt = device.kcrs_to_crsk(kernels.filters_to_device_kcrs(filters))
-    y = device.si_conv(nodes, seg, 1, c, h, w, wt, len(filters), h_f, w_f, stride, padding)
+    kcrs = kernels.filters_to_device_kcrs(filters)
+    if (h_f, w_f, stride, padding) == (3, 3, 1, 1):
+        y = device.si_conv3x3(nodes, seg, 1, c, h, w, device.si_pack3x3(kcrs), len(filters))
+    else:
+        y = device.si_conv(nodes, seg, 1, c, h, w, device.kcrs_to_crsk(kcrs), len(filters), h_f, w_f, stride, padding)
     return y, geom
 
 

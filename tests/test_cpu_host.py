@@ -120,11 +120,11 @@ def test_multiply_count_matches_oracle(oracle):
 def test_launch_planner():
     assert device.pick_ly(224) == 8 and device.pick_ly(112) == 4 and device.pick_ly(56) == 2
     counts = np.full((16, 512), 5, np.int64)  # 16 groups x 512 channels, 4 nodes + sentinel
-    bank = device.PackedBank(64, 512, None, None, int(counts.sum()), counts, 0)
+    bank = device.PackedBank(64, 512, 4, None, None, int(counts.sum()), counts, 0)
     cc, mx = bank.chunk_plan(8)
     assert cc == 8 and mx == 40
     assert device.sf3x3_smem_bytes(8, cc, mx + 4, 512) <= device.SMEM_LIMIT
-    dense = device.PackedBank(64, 512, None, None, 0, np.full((16, 512), 37, np.int64), 0)
+    dense = device.PackedBank(64, 512, 4, None, None, 0, np.full((16, 512), 37, np.int64), 0)
     cc2, mx2 = dense.chunk_plan(2)  # a fully dense bank still fits (smaller chunks if needed)
     assert device.sf3x3_smem_bytes(2, cc2, mx2 + 4, 512) <= device.SMEM_LIMIT
 

@@ -172,6 +172,36 @@ def test_si_conv_matches_reference_bitwise(dev, oracle):
         assert np.array_equal(y.view(np.int32), g[f"c{i}__y"].view(np.int32)), i
 
 
+def test_si_strip_kernel_bitwise(dev, oracle):
+    """3x3/s1/p1 strip kernel == reference order, bit for bit (incl. ragged widths)."""
+    g = load_golden("si_conv.npz")
+    hit = 0
+    for i in range(int(g["n_cases"])):
+        x, w, bias = g[f"c{i}__x"], g[f"c{i}__w"], g[f"c{i}__bias"]
+        s, p = (int(v) for v in g[f"c{i}__geom"])
+        if w.shape[2:] != (3, 3) or (s, p) != (1, 1):
+            continue
+        hit += 1
+        enc = dev.encode_order(_t(x[None]), "CHW")
+        dense = str(g[f"c{i}__kind"]) == "dense"
+        y = dev.si_conv3x3(enc.nodes, enc.seg_off, 1, *x.shape, dev.si_pack3x3(_t(w)), w.shape[0],
+                           _t(bias) if dense else None).cpu().numpy()[0]
+        assert np.array_equal(y.view(np.int32), g[f"c{i}__y"].view(np.int32)), i
+    assert hit >= 3
+    rng = np.random.default_rng(12)
+    for (n, c, k, h, wd) in ((2, 37, 70, 13, 29), (1, 5, 3, 1, 1), (3, 64, 33, 28, 28)):
+        x = np.abs(rng.standard_normal((n, c, h, wd))).astype(np.float32)
+        x[rng.random(x.shape) < 0.8] = 0
+        wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+        enc = dev.encode_order(_t(x), "CHW")
+        got = dev.si_conv3x3(enc.nodes, enc.seg_off, n, c, h, wd, dev.si_pack3x3(_t(wt)), k).cpu().numpy()
+        ref = dev.si_conv(enc.nodes, enc.seg_off, n, c, h, wd, dev.kcrs_to_crsk(_t(wt)), k, 3, 3, 1, 1).cpu().numpy()
+        assert np.array_equal(got.view(np.int32), ref.view(np.int32))
+        segs = [oracle.encode(x[b], "CHW") for b in range(n)]
+        oref = oracle.si_conv([s[0] for s in segs], [s[2] for s in segs], (c, h, wd), wt, 1, 1)
+        assert np.array_equal(got, oref)
+
+
 def test_si_conv_config2(dev):
     import hashlib
 
@@ -180,6 +210,8 @@ def test_si_conv_config2(dev):
     enc = dev.encode_order(_t(x), "CHW")
     y = dev.si_conv(enc.nodes, enc.seg_off, 1, 128, 28, 28, dev.kcrs_to_crsk(_t(w)), 128, 3, 3, 1, 1)
     assert np.array_equal(y.cpu().numpy()[0], g["y"])
+    y2 = dev.si_conv3x3(enc.nodes, enc.seg_off, 1, 128, 28, 28, dev.si_pack3x3(_t(w)), 128)
+    assert np.array_equal(y2.cpu().numpy()[0], g["y"])
     out = dev.encode_order(y, "CHW")
     h = hashlib.sha256()
     for a in (out.nodes[: out.n_nodes].cpu().numpy(), out.matrix_off.cpu().numpy(), out.seg_off.cpu().numpy()):

@@ -89,11 +89,11 @@ def main():
         for zf in (0.5, 0.75, 0.9, 0.95):
             x, wt, b = wl.sweep_layer(li, "si", zf, n=args.n)
             xd = torch.from_numpy(x).cuda()
-            wcrsk = device.kcrs_to_crsk(torch.from_numpy(wt).cuda())
+            wq = device.si_pack3x3(torch.from_numpy(wt).cuda())
             enc = device.encode_order(xd, "CHW")
             out = torch.empty((args.n, k, h, w), dtype=torch.float32, device="cuda")
-            ms = time_fn(lambda: device.si_conv(enc.nodes, enc.seg_off, args.n, c, h, w, wcrsk, k, 3, 3, 1, 1,
-                                                out=out), args.reps)
+            ms = time_fn(lambda: device.si_conv3x3(enc.nodes, enc.seg_off, args.n, c, h, w, wq, k, out=out),
+                         args.reps)
             fl = si_flops(x, k)
             r = {"mode": "si", "layer": li, "shape": [c, k, h, w], "zero_frac": zf, "ms": ms,
                  "nnz_gflop": fl / 1e9, "tflops": fl / (ms * 1e-3) / 1e12}
