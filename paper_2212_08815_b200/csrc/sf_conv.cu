@@ -72,7 +72,11 @@ __global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, i
 // ------------------------------------------------------------------------------
 // KT filters per warp (4 or 8, == the pack's kt); a CTA always holds 32 filters:
 // KT=4 -> 8 warps (<=128 regs, 2 CTAs = 16 warps/SM), KT=8 -> 4 warps (2 CTAs = 8 warps/SM)
-constexpr int CTA_FILTERS = 32;
+#ifndef FSCNN_SF3_CTA_FILTERS
+#define FSCNN_SF3_CTA_FILTERS 32
+#endif
+constexpr int CTA_FILTERS = FSCNN_SF3_CTA_FILTERS;
+constexpr int CTAS_PER_SM = CTA_FILTERS == 32 ? 2 : 1;
 template <int KT> struct SfCfg {
     static constexpr int NWARP = CTA_FILTERS / KT;
     static constexpr int NTHREADS = NWARP * 32;
@@ -152,7 +156,7 @@ struct Sf3Params {
 };
 
 template <int LY, int KT>
-__global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, 2)
+__global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
     constexpr int NWARP = SfCfg<KT>::NWARP;
     constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
@@ -386,7 +390,8 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     };
     // deepest ring that still lets two CTAs share an SM (228 KB, 1 KB reserved each)
     p.stages = MAX_STAGES;
-    while (p.stages > 2 && smem_for(p.stages) > 113 * 1024) --p.stages;
+    const size_t budget = CTAS_PER_SM == 2 ? 113 * 1024 : 227 * 1024;
+    while (p.stages > 2 && smem_for(p.stages) > budget) --p.stages;
     size_t smem = smem_for(p.stages);
     if (smem > 227 * 1024) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
