@@ -17,13 +17,19 @@ Arithmetic: accumulators and the patch are held as 64-bit register pairs
 (two adjacent columns).  Taps with kw in {0, 2} read column-aligned pairs and run as
 8 FFMA2 (fma.rn.f32x2: two FP32 FMAs per instruction, same FMA-pipe rate, half the
 issue slots); kw = 1 straddles the pairs and runs as 16 scalar FFMA on the halves.
-The next entry is prefetched one step ahead.
+The next entry is loaded at the top of each case (overlapping its FMAs).
+
+Measured alternatives (tools/brx_bench.cu, B200): a 7-level compare-and-branch tree
+instead of brx.idx is ~60 cycles/nonzero slower; replicating the dispatch at the end of
+every case (no jump back to N_) is ~20% slower; loading the next entry before the BRX
+instead of inside the case is ~3% slower.
 
 Operands (all via the C++ wrapper sf3x3_chunk below; NA = 8*KT):
   %0..%NA-1     acc pairs  acc2[kl][py][h]  (kl*8 + py*2 + h), h=0: cols 0,1  h=1: cols 2,3
   next 18       patch pairs pt2[r][h]        (r*3 + h),         h: cols 2h, 2h+1
   then          entry cursor, patch cursor (shared addresses), channels left in the chunk,
-                channel pitch of a staged box in bytes (immediate; row pitch is 80 B)
+                channel pitch of a staged box in bytes (register), row pitch in bytes
+                (immediate, template parameter ROW_BYTES)
 
 Run: python gen_sf3x3_dispatch.py > sf3x3_dispatch.inc
 """
@@ -31,20 +37,20 @@ Run: python gen_sf3x3_dispatch.py > sf3x3_dispatch.inc
 TILE, PATCH = 4, 6
 
 
-ROW_BYTES = 80  # smem row pitch of a staged box: 20 floats (BOXW in sf_conv.cu)
 
 
-def load_patch(e, P, PP):
+def load_patch(e, P, PP, RB):
+    # RB: the row pitch operand (an immediate; PTX folds the constant expression)
     for r in range(PATCH):
-        e(f"ld.shared.v2.b64 {{{P(r, 0)}, {P(r, 1)}}}, [{PP}+{r * ROW_BYTES}];")
-        e(f"ld.shared.b64 {P(r, 2)}, [{PP}+{r * ROW_BYTES + 16}];")
+        e(f"ld.shared.v2.b64 {{{P(r, 0)}, {P(r, 1)}}}, [{PP}+{RB}*{r}];")
+        e(f"ld.shared.b64 {P(r, 2)}, [{PP}+{RB}*{r}+16];")
 
 
 def block(KT: int) -> str:
     NA = KT * 8                                              # acc pair operands
     A = lambda kl, py, h: f"%{kl * 8 + py * 2 + h}"          # acc pair
     P = lambda r, h: f"%{NA + r * 3 + h}"                    # patch pair
-    CUR, PP, CNT, CHS = (f"%{NA + 18 + i}" for i in range(4))
+    CUR, PP, CNT, CHS, RB = (f"%{NA + 18 + i}" for i in range(5))
     NC = KT * 9
     L = []
     e = L.append
@@ -56,16 +62,20 @@ def block(KT: int) -> str:
     # targets: 0..NC-1 entry, NC..2NC-1 channel-last entry, 2NC empty channel
     targets = ", ".join([f"C{i}_%=" for i in range(NC)] + [f"X{i}_%=" for i in range(NC)] + ["E_%="])
     e(f"T_%=: .branchtargets {targets};")
-    load_patch(e, P, PP)
+    load_patch(e, P, PP, RB)
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
     e(f"add.u32 {CUR}, {CUR}, 8;")
     e("N_%=:")
     e("mov.b32 f_v, r_v1;")
     e("mov.b32 r_ix, r_i1;")
     e("mov.b64 d_vv, {r_v1, r_v1};")
-    e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
-    e(f"add.u32 {CUR}, {CUR}, 8;")
     e("brx.idx.uni r_ix, T_%=;")
+
+    def prefetch():
+        # the next entry is loaded at the top of each case, so the load overlaps the case's
+        # FMAs (ptxas makes BRX wait on every outstanding scoreboard)
+        e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
+        e(f"add.u32 {CUR}, {CUR}, 8;")
 
     def fmas(kl, tap):
         kh, kw = divmod(tap, 3)
@@ -94,11 +104,13 @@ def block(KT: int) -> str:
     for kl in range(KT):
         for tap in range(9):
             e(f"C{kl * 9 + tap}_%=:")
+            prefetch()
             fmas(kl, tap)
             e("bra.uni N_%=;")
     for kl in range(KT):
         for tap in range(9):
             e(f"X{kl * 9 + tap}_%=:")
+            prefetch()
             fmas(kl, tap)
             e("bra.uni S_%=;")
     # channel-last entry: the prefetched slot was the segment's sentinel; skip it
@@ -107,17 +119,18 @@ def block(KT: int) -> str:
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
     e("@p_end bra.uni D_%=;")
     e(f"add.u32 {PP}, {PP}, {CHS};")
-    load_patch(e, P, PP)
+    load_patch(e, P, PP, RB)
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
     e(f"add.u32 {CUR}, {CUR}, 8;")
     e("bra.uni N_%=;")
     # empty channel: the prefetched entry already belongs to the next channel
     e("E_%=:")
+    prefetch()
     e(f"sub.u32 {CNT}, {CNT}, 1;")
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
     e("@p_end bra.uni D_%=;")
     e(f"add.u32 {PP}, {PP}, {CHS};")
-    load_patch(e, P, PP)
+    load_patch(e, P, PP, RB)
     e("bra.uni N_%=;")
     e("D_%=:")
     e("}")
@@ -127,15 +140,16 @@ def block(KT: int) -> str:
 def emit(KT: int) -> None:
     outs = ", ".join(f'"+l"(acc2[{kl}][{py}][{h}])' for kl in range(KT) for py in range(TILE) for h in range(2))
     pts = ", ".join(f'"=l"(pt2[{r}][{h}])' for r in range(PATCH) for h in range(3))
-    print("template <int CH_BYTES>")
+    print("template <int ROW_BYTES>")
     print(f"__device__ __forceinline__ void sf3x3_chunk(unsigned long long (&acc2)[{KT}][4][2],")
-    print("                                            uint32_t cur, uint32_t patch, uint32_t n_ch) {")
+    print("                                            uint32_t cur, uint32_t patch, uint32_t n_ch,")
+    print("                                            uint32_t ch_bytes) {")
     print("    unsigned long long pt2[6][3];")
     print(f'    asm volatile("{block(KT)}"')
     print(f"                 : {outs},")
     print(f"                   {pts},")
     print('                   "+r"(cur), "+r"(patch), "+r"(n_ch)')
-    print('                 : "n"(CH_BYTES)')
+    print('                 : "r"(ch_bytes), "n"(ROW_BYTES)')
     print('                 : "memory");')
     print("}")
     print()

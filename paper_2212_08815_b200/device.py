@@ -145,12 +145,33 @@ def _align(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4) -> int:
+FLAT = -1  # sub-region "height" selecting the flat mode (sf_conv.cu: LY = 0)
+SMEM_2CTA = 113 * 1024  # per-CTA budget that keeps two CTAs resident per SM
+
+
+def flat_geometry(h: int, w: int):
+    """(tiles_h, tiles_w, box pitch, box rows) of the flat mode, or None when it does not
+    apply (mirrors flat_geometry in sf_conv.cu)."""
+    tw, th = math.ceil(w / TILE), math.ceil(h / TILE)
+    need = TILE * tw + 2
+    pitch = 36 if need <= 36 else (60 if need <= 60 else 0)
+    tpi = tw * th
+    if not pitch or not (tpi >= 32 or tpi == 16):
+        return None
+    ntr = min(th, (tw + 30) // tw + 1)
+    return th, tw, pitch, TILE * ntr + 2
+
+
+def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4, h: int = 0, w: int = 0,
+                     stages: int = STAGES) -> int:
     NWARP = CTA_FILTERS // kt
-    li = 8 // ly
-    box = _align(BOXW * (TILE * ly + 2) * cc, 32)
+    if ly == FLAT:
+        _, _, pitch, box_h = flat_geometry(h, w)
+        li, box = 2, _align(pitch * box_h * cc, 32)
+    else:
+        li, box = 8 // ly, _align(BOXW * (TILE * ly + 2) * cc, 32)
     n_chunks = math.ceil(c / cc)
-    return (STAGES * li * box * 4 + STAGES * NWARP * ent_cap * 8 + 2 * STAGES * 8
+    return (stages * li * box * 4 + stages * NWARP * ent_cap * 8 + 2 * stages * 8
             + NWARP * (n_chunks + 1) * 4)
 
 
@@ -163,6 +184,19 @@ def pick_ly(h: int) -> int:
         if best is None or key < best[0]:
             best = (key, ly)
     return best[1]
+
+
+def pick_layout(n: int, h: int, w: int) -> int:
+    """Rectangular sub-region height (pick_ly), or FLAT when the flat mode idles clearly
+    fewer lanes (mirrors the auto rule of fscnn_sf_conv3x3_ex)."""
+    ly = pick_ly(h)
+    geo = flat_geometry(h, w)
+    if geo is None:
+        return ly
+    th, tw, _, _ = geo
+    rect = h * w / (math.ceil(h / (TILE * ly)) * TILE * ly * math.ceil(w / SUBW) * SUBW)
+    flat = n * h * w / (math.ceil(n * th * tw / 32) * 32 * 16)
+    return FLAT if flat > 1.03 * rect else ly
 
 
 @dataclass
@@ -179,15 +213,18 @@ class PackedBank:
     nnz: int                   # nonzero weights
     _cache: dict = None
 
-    def chunk_plan(self, ly: int) -> tuple[int, int]:
-        """(cc, max_chunk_entries) fitting shared memory for sub-region height ly."""
+    def chunk_plan(self, ly: int, h: int = 0, w: int = 0) -> tuple[int, int]:
+        """(cc, max_chunk_entries) for layout ly (FLAT needs h, w): the largest channel
+        chunk whose 2-stage ring keeps two CTAs per SM, else the largest that fits at all."""
+        key = (ly, h, w) if ly == FLAT else ly
         if self._cache is None:
             self._cache = {}
-        if ly in self._cache:
-            return self._cache[ly]
+        if key in self._cache:
+            return self._cache[key]
         import os
 
         forced = int(os.environ.get("FSCNN_SF3_CC", "0"))
+        cands = []
         for cc in ((forced,) if forced else (8, 4, 2, 1)):
             if cc > self.c and cc != 1 and not forced:
                 continue
@@ -196,9 +233,12 @@ class PackedBank:
             cnt = np.pad(self.counts, ((0, 0), (0, pad)))
             mx = int(cnt.reshape(cnt.shape[0], n_chunks, cc).sum(axis=2).max())
             ent_cap = (mx + 4) & ~1
-            if sf3x3_smem_bytes(ly, cc, ent_cap, self.c, self.kt) <= SMEM_LIMIT:
-                self._cache[ly] = (cc, mx)
-                return cc, mx
+            cands.append((cc, mx, sf3x3_smem_bytes(ly, cc, ent_cap, self.c, self.kt, h, w)))
+        for limit in (SMEM_2CTA, SMEM_LIMIT):
+            for cc, mx, need in cands:
+                if need <= limit:
+                    self._cache[key] = (cc, mx)
+                    return cc, mx
         raise RuntimeError("filter bank too dense for the fast kernel's shared memory")
 
 
@@ -273,9 +313,9 @@ def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, rel
     w = ldi - 1 if w is None else int(w)
     assert x.stride(3) == 1 and x.stride(1) == ldi * h and x.stride(0) == ldi * h * c
     assert c == bank.c and ldi >= w + 1
-    if ly <= 0:
-        ly = pick_ly(h)
-    cc, mx = bank.chunk_plan(ly)
+    if ly == 0:
+        ly = pick_layout(n, h, w)
+    cc, mx = bank.chunk_plan(ly, h, w)
     ho, wo = (h // 2, w // 2) if pool else (h, w)
     if out is None:
         out = halo_empty(n, bank.k, ho, wo, x.device)

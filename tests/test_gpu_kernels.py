@@ -118,6 +118,12 @@ def test_sf_fast_config1_within_tolerance(dev):
         (1, 17, 8, 9, 23, 0.0, 4),
         (2, 8, 130, 40, 36, 0.95, 8),
         (1, 5, 3, 1, 1, 0.0, 0),
+        # flat mode (ly = -1): CTAs straddle images, ragged widths, both box pitches
+        (3, 20, 40, 28, 28, 0.9, -1),
+        (2, 16, 32, 56, 56, 0.9, -1),
+        (4, 8, 12, 14, 14, 0.5, -1),
+        (2, 9, 16, 27, 30, 0.8, -1),
+        (1, 12, 8, 50, 41, 0.9, -1),
     ],
 )
 def test_sf_fast_matches_oracle(dev, oracle, n, c, k, h, w, zf, ly):
@@ -140,6 +146,23 @@ def test_sf_fast_matches_oracle(dev, oracle, n, c, k, h, w, zf, ly):
         yp = dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=True, w=w, ly=ly)
         want = oracle.pool(oracle.relu(ref), 2, 2, "max")
         assert normwise_err(dev.from_halo(yp, w // 2).cpu().numpy(), want) <= FAST_TOL
+
+
+@pytest.mark.parametrize("n,h,w,ly", [(3, 28, 28, 2), (2, 56, 56, 2), (5, 14, 14, 2), (2, 27, 30, 4)])
+def test_sf_fast_flat_equals_rect_bitwise(dev, n, h, w, ly):
+    """Both lane mappings run the same per-lane arithmetic: outputs are bit-identical."""
+    rng = np.random.default_rng(h * w + n)
+    x = rng.standard_normal((n, 24, h, w)).astype(np.float32)
+    wt = rng.standard_normal((36, 24, 3, 3)).astype(np.float32)
+    wt[rng.random(wt.shape) < 0.9] = 0
+    bias = rng.standard_normal(36).astype(np.float32)
+    bank = dev.sf_pack(_t(wt))
+    xp = dev.to_halo(_t(x))
+    for pool in ((False, True) if h % 2 == 0 and w % 2 == 0 else (False,)):
+        a = dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=w, ly=ly)
+        b = dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=w, ly=dev.FLAT)
+        wo = w // 2 if pool else w
+        assert dev.from_halo(a, wo).cpu().numpy().tobytes() == dev.from_halo(b, wo).cpu().numpy().tobytes()
 
 
 def test_sf_fast_is_deterministic_and_batch_invariant(dev):
