@@ -142,9 +142,8 @@ struct Sf3Params {
     int n, c, h, w;           // input extents (NCHW, row pitch = TMA stride)
     int k;                    // output channels
     int ldo;                  // output row pitch (floats)
-    int tiles_h, tiles_w;     // sub-region grid per image (flat mode: lane-tile grid)
-    int n_sub;                // n * tiles_h * tiles_w (flat mode: total lane tiles)
-    int box_h;                // flat mode: staged rows per image part
+    int tiles_h, tiles_w;     // sub-region grid per image
+    int n_sub;                // n * tiles_h * tiles_w
     int cc;                   // channels per chunk
     int ent_cap;              // entry slots per warp per stage (int2)
     int box_floats;           // floats per sub-region box per stage
@@ -153,26 +152,17 @@ struct Sf3Params {
     int relu;
     int pool;                 // fused 2x2 max-pool
     int stages;               // ring depth (<= MAX_STAGES)
-    int dbg;                  // debug: 1 = skip compute, 3 = no TMA, 4 = no bulk copies (1,3,4 skip compute);
-                              // 5 = compute without box TMA, 6 = compute on the first STAGES chunks' data only
+    int dbg;                  // debug: 1 = skip compute, 3 = no TMA, 4 = no bulk copies (1,3,4 skip compute)
 };
 
-// LY > 0: rectangular mode -- the CTA's 32 lane tiles form LI = 8/LY sub-regions of
-//         (4*LY) x 16 outputs, one TMA box each (row pitch BW = BOXW).
-// LY = 0: flat mode for narrow layers -- the CTA takes 32 consecutive lane tiles of the
-//         batch's (image, tile row, tile col) enumeration, so no lane idles when the
-//         width is not a multiple of 16 (56 -> 12.5% idle, 28 -> 23% idle in the
-//         rectangular mode); one full-width box of box_h rows per image part (a CTA
-//         spans at most two images), row pitch BW >= w + 2 rounded to 4.
-template <int LY, int KT, int BW>
+template <int LY, int KT>
 __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
     constexpr int NWARP = SfCfg<KT>::NWARP;
     constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
-    constexpr bool FLAT = LY == 0;
-    constexpr int LI = FLAT ? 2 : 8 / LY;       // boxes per stage (sub-regions / image parts)
-    constexpr int SUBH = FLAT ? 0 : TILE * LY;  // sub-region height (rectangular mode)
-    const int BOXH = FLAT ? p.box_h : SUBH + 2;
+    constexpr int LI = 8 / LY;          // sub-regions per CTA
+    constexpr int SUBH = TILE * LY;     // sub-region height
+    constexpr int BOXH = SUBH + 2;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float *in_s = reinterpret_cast<float *>(smem_raw);
     const int STAGES = p.stages;
@@ -184,13 +174,6 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub0 = blockIdx.x * LI;
-    // flat mode: this CTA's tiles [t0, t1], first image and its first tile row
-    const int tpi = p.tiles_h * p.tiles_w;
-    const int t0 = blockIdx.x * 32;
-    const int t1 = min(t0 + 31, p.n_sub - 1);
-    const int img0 = FLAT ? t0 / tpi : 0;
-    const int tr0 = FLAT ? (t0 % tpi) / p.tiles_w : 0;
-    const bool cross = FLAT && (t1 / tpi != img0);
     const int g0 = blockIdx.y * NWARP;
     const int n_groups = (p.k + KT - 1) / KT;
     const int n_chunks = (p.c + p.cc - 1) / p.cc;
@@ -221,14 +204,10 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     const int g = g0 + warp;
     const bool live = g < n_groups;
     int n_box = 0;
-    if (FLAT) {
-        n_box = cross ? 2 : 1;
-    } else {
 #pragma unroll
-        for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
-    }
+    for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
     const uint32_t box_bytes =
-        (p.dbg == 3 || p.dbg == 5) ? 0u : (uint32_t)n_box * (uint32_t)(BW * BOXH * p.cc * 4);
+        (p.dbg == 3) ? 0u : (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
 
     // Each warp stages its own entry run for chunk ch (lane 0); dead groups arrive empty.
     auto refill_entries = [&](int ch) {
@@ -248,16 +227,7 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     auto refill_boxes = [&](int ch) {
         const int s = ch % STAGES;
         mbar_expect_tx(&full[s], box_bytes);
-        if (p.dbg == 3 || p.dbg == 5) return;
-        if (FLAT) {
-            // part 0: rows from tile row tr0 of image img0; part 1: the next image from row 0
-            // (full width from memory column 0 = logical column -1; rows beyond the image
-            // and columns beyond w are zero-filled by the TMA unit)
-            float *dst = in_s + s * stage_in_floats;
-            tma_load_4d(dst, &tmap, &full[s], 0, TILE * tr0 - 1, ch * p.cc, img0);
-            if (cross) tma_load_4d(dst + p.box_floats, &tmap, &full[s], 0, -1, ch * p.cc, img0 + 1);
-            return;
-        }
+        if (p.dbg == 3) return;
 #pragma unroll
         for (int li = 0; li < LI; ++li) {
             int sub = sub0 + li;
@@ -281,36 +251,9 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
         }
     __syncwarp();  // the dispatch loop's .uni branches need a converged warp
 
-    // this lane's tile: image, output origin (y0, x0), and its patch origin in a box
-    int img, y0, x0, box_id, box_row;
-    bool lane_live;
-    if (FLAT) {
-        const int t = t0 + lane;
-        lane_live = t < p.n_sub;
-        const int tt = lane_live ? t : t0;
-        img = tt / tpi;
-        const int rem = tt % tpi;
-        const int tr = rem / p.tiles_w, tc = rem % p.tiles_w;
-        box_id = img - img0;
-        box_row = TILE * (box_id ? tr : tr - tr0);
-        y0 = TILE * tr;
-        x0 = TILE * tc;
-    } else {
-        constexpr int LYD = FLAT ? 1 : LY;
-        const int lx = lane & 3;
-        const int ly = (lane >> 2) % LYD;
-        box_id = lane / (4 * LYD);
-        box_row = TILE * ly;
-        const int sub = sub0 + box_id;
-        lane_live = sub < p.n_sub;
-        const int tw = sub % p.tiles_w;
-        const int r = sub / p.tiles_w;
-        const int th = r % p.tiles_h;
-        img = r / p.tiles_h;
-        y0 = th * SUBH + TILE * ly;
-        x0 = tw * SUBW + TILE * lx;
-    }
-    const int box_col = FLAT ? x0 : x0 % SUBW;  // memory column x0 + 1 - 1: box starts at logical -1
+    const int lx = lane & 3;
+    const int ly = (lane >> 2) % LY;
+    const int li = lane / (4 * LY);
 
     // accumulators as column pairs (FFMA2 operands): acc2[kl][py][h] = cols 2h, 2h+1
     unsigned long long acc2[KT][TILE][2];
@@ -322,21 +265,22 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
 #pragma unroll 1
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int s = ch % STAGES;
-        if (p.dbg != 6 || ch < STAGES) mbar_wait(&full[s], (ch / STAGES) & 1);
+        mbar_wait(&full[s], (ch / STAGES) & 1);
         __syncwarp();
         const int c0 = ch * p.cc;
         const int cnt = min(p.cc, p.c - c0);
-        if (live && (p.dbg == 0 || p.dbg >= 5)) {
+        if (live && p.dbg == 0) {
             const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
             const int e0 = cofs[warp * (n_chunks + 1) + ch] & 1;  // offset inside aligned copy
-            const float *box = in_s + s * stage_in_floats + box_id * p.box_floats;
-            sf3x3_chunk<BW * 4>(acc2, smem_u32(ents + e0), smem_u32(box + box_row * BW + box_col),
-                                cnt, (uint32_t)(BOXH * BW * 4));
+            const float *box = in_s + s * stage_in_floats + li * p.box_floats;
+            sf3x3_chunk<BOXW * 4>(acc2, smem_u32(ents + e0),
+                                  smem_u32(box + (TILE * ly) * BOXW + TILE * lx), cnt,
+                                  (uint32_t)(BOXH * BOXW * 4));
         }
         __syncwarp();
         // Stage s is free for this warp: restage its own entry run for chunk ch+STAGES;
         // the last warp to leave the stage also restages the shared input boxes.
-        if (lane == 0 && ch + STAGES < n_chunks && p.dbg != 6) {
+        if (lane == 0 && ch + STAGES < n_chunks) {
             refill_entries(ch + STAGES);
             // the counter only grows: every NWARP-th arrival closes a round
             if ((atomicAdd(&done[s], 1) + 1) % NWARP == 0) refill_boxes(ch + STAGES);
@@ -345,7 +289,14 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     }
 
     // ---------------- epilogue ----------------
-    if (g >= n_groups || !lane_live) return;
+    const int sub = sub0 + li;
+    if (g >= n_groups || sub >= p.n_sub) return;
+    const int tw = sub % p.tiles_w;
+    const int r = sub / p.tiles_w;
+    const int th = r % p.tiles_h;
+    const int img = r / p.tiles_h;
+    const int y0 = th * SUBH + TILE * ly;
+    const int x0 = tw * SUBW + TILE * lx;
     if (y0 >= p.h || x0 >= p.w) return;
 #pragma unroll
     for (int kl = 0; kl < KT; ++kl) {
@@ -421,39 +372,14 @@ EncodeTiledFn get_encode_tiled() {
     return fn;
 }
 
-// Flat-mode geometry (LY = 0): lane-tile grid, row pitch BW of the staged boxes and rows
-// per image part.  Returns false when the flat mode does not apply (too wide, or a CTA
-// could span more than two images).
-bool flat_geometry(int h, int w, int *tiles_h, int *tiles_w, int *bw, int *box_h) {
-    const int tw = (int)ceil_div(w, TILE), th = (int)ceil_div(h, TILE);
-    const int need = TILE * tw + 2;  // patch columns of the last tile column
-    const int pitch = need <= 36 ? 36 : (need <= 60 ? 60 : 0);
-    const int tpi = tw * th;
-    if (!pitch || !(tpi >= 32 || tpi == 16)) return false;
-    const int ntr = min(th, (tw + 30) / tw + 1);  // tile rows 32 consecutive tiles can touch
-    *tiles_h = th; *tiles_w = tw; *bw = pitch; *box_h = TILE * ntr + 2;
-    return true;
-}
-
-template <int LY, int KT, int BW>
+template <int LY, int KT>
 int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
-    constexpr bool FLAT = LY == 0;
-    constexpr int LI = FLAT ? 2 : 8 / LY;
-    constexpr int SUBH = FLAT ? 0 : TILE * LY;
-    int lanes_per_cta_unit = LI;  // grid.x covers n_sub in units of LI (rect) or 32 tiles (flat)
-    if (FLAT) {
-        int bw;
-        flat_geometry(p.h, p.w, &p.tiles_h, &p.tiles_w, &bw, &p.box_h);
-        p.n_sub = p.n * p.tiles_h * p.tiles_w;
-        p.box_floats = BW * p.box_h * p.cc;
-        lanes_per_cta_unit = 32;
-    } else {
-        p.tiles_h = (int)ceil_div(p.h, SUBH);
-        p.tiles_w = (int)ceil_div(p.w, SUBW);
-        p.n_sub = p.n * p.tiles_h * p.tiles_w;
-        p.box_h = SUBH + 2;
-        p.box_floats = BOXW * (SUBH + 2) * p.cc;
-    }
+    constexpr int LI = 8 / LY;
+    constexpr int SUBH = TILE * LY;
+    p.tiles_h = (int)ceil_div(p.h, SUBH);
+    p.tiles_w = (int)ceil_div(p.w, SUBW);
+    p.n_sub = p.n * p.tiles_h * p.tiles_w;
+    p.box_floats = BOXW * (SUBH + 2) * p.cc;
     // each box must start 128-byte aligned (TMA destination)
     p.box_floats = (p.box_floats + 31) & ~31;
     constexpr int NWARP = SfCfg<KT>::NWARP;
@@ -472,21 +398,16 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
         return FSCNN_ERR_UNSUPPORTED;
     }
-    auto kern = sf3x3_kernel<LY, KT, BW>;
+    auto kern = sf3x3_kernel<LY, KT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("sf3x3: smem attribute (%zu bytes): %s", smem, cudaGetErrorString(e));
         return FSCNN_ERR_CUDA;
     }
     int n_groups = (int)ceil_div(p.k, KT);
-    dim3 grid((unsigned)ceil_div(p.n_sub, lanes_per_cta_unit), (unsigned)ceil_div(n_groups, NWARP));
+    dim3 grid((unsigned)ceil_div(p.n_sub, LI), (unsigned)ceil_div(n_groups, NWARP));
     kern<<<grid, NTHREADS, smem, st>>>(map, p);
     return check_launch("sf3x3_kernel");
-}
-
-// Lane utilisation of the rectangular mode with sub-region height 4*ly.
-double rect_util(int h, int w, int ly) {
-    return (double)h * w / ((double)ceil_div(h, TILE * ly) * TILE * ly * ceil_div(w, SUBW) * SUBW);
 }
 
 }  // namespace
@@ -547,28 +468,15 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
     p.ent_cap = (max_chunk_entries + 3 + 1) & ~1;
     p.bias = bias; p.y = y; p.relu = relu; p.pool = pool;
     p.dbg = dbg_mode;
-    int fth, ftw, fbw = 0, fbox_h = 0;
-    const bool flat_ok = flat_geometry(h, w, &fth, &ftw, &fbw, &fbox_h);
-    if (ly == 0) {
-        // auto: the rectangular height with the fewest padded rows, or the flat mode when
-        // it idles clearly fewer lanes
-        ly = 8;
-        for (int cand : {8, 4, 2})
-            if (ceil_div(h, TILE * cand) * TILE * cand < ceil_div(h, TILE * ly) * TILE * ly) ly = cand;
-        if (flat_ok) {
-            const double tiles = (double)n * fth * ftw;
-            const double flat_util = (double)n * h * w / (ceil_div((int64_t)tiles, 32) * 32.0 * 16.0);
-            if (flat_util > 1.03 * rect_util(h, w, ly)) ly = -1;
-        }
-    }
-    if (ly < 0) FSCNN_REQUIRE(flat_ok, "flat mode needs w <= 56 and >= 16 lane tiles per image");
-    const int box_w = ly < 0 ? fbw : BOXW;
-    const int box_h = ly < 0 ? fbox_h : TILE * ly + 2;
+    // auto: 16x16 sub-regions (measured fastest on every VGG16 width at 16-channel
+    // chunks); 8x16 for very shallow inputs or short images
+    if (ly <= 0) ly = (c < 8 || h <= 8) ? 2 : 4;
+    int sub_h = TILE * ly;
     CUtensorMap map;
     cuuint64_t gdim[4] = {(cuuint64_t)w + 1, (cuuint64_t)h, (cuuint64_t)c, (cuuint64_t)n};
     cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * h * 4,
                              (cuuint64_t)ldi * h * c * 4};
-    cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)box_h, (cuuint32_t)cc, 1};
+    cuuint32_t box[4] = {(cuuint32_t)BOXW, (cuuint32_t)(sub_h + 2), (cuuint32_t)cc, 1};
     cuuint32_t estride[4] = {1, 1, 1, 1};
     CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride,
                      box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -578,18 +486,13 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
         return FSCNN_ERR_CUDA;
     }
     cudaStream_t st = as_stream(stream);
-    const int mode = ly < 0 ? (fbw == 36 ? 100 : 101) : ly;
-    switch (mode * 16 + kt) {
-        case 8 * 16 + 4: return launch_sf3x3<8, 4, BOXW>(map, p, st);
-        case 4 * 16 + 4: return launch_sf3x3<4, 4, BOXW>(map, p, st);
-        case 2 * 16 + 4: return launch_sf3x3<2, 4, BOXW>(map, p, st);
-        case 100 * 16 + 4: return launch_sf3x3<0, 4, 36>(map, p, st);
-        case 101 * 16 + 4: return launch_sf3x3<0, 4, 60>(map, p, st);
-        case 8 * 16 + 8: return launch_sf3x3<8, 8, BOXW>(map, p, st);
-        case 4 * 16 + 8: return launch_sf3x3<4, 8, BOXW>(map, p, st);
-        case 2 * 16 + 8: return launch_sf3x3<2, 8, BOXW>(map, p, st);
-        case 100 * 16 + 8: return launch_sf3x3<0, 8, 36>(map, p, st);
-        case 101 * 16 + 8: return launch_sf3x3<0, 8, 60>(map, p, st);
+    switch (ly * 16 + kt) {
+        case 8 * 16 + 4: return launch_sf3x3<8, 4>(map, p, st);
+        case 4 * 16 + 4: return launch_sf3x3<4, 4>(map, p, st);
+        case 2 * 16 + 4: return launch_sf3x3<2, 4>(map, p, st);
+        case 8 * 16 + 8: return launch_sf3x3<8, 8>(map, p, st);
+        case 4 * 16 + 8: return launch_sf3x3<4, 8>(map, p, st);
+        case 2 * 16 + 8: return launch_sf3x3<2, 8>(map, p, st);
         default: set_error("unsupported sub-region height %d / kt %d", ly, kt); return FSCNN_ERR_ARG;
     }
 }

@@ -137,7 +137,9 @@ def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None
 # -- sparse-filter conv ------------------------------------------------------------------
 
 STAGES, BOXW, SUBW, TILE = 2, 20, 16, 4  # STAGES: the minimum ring the kernel runs with
-CTA_FILTERS = 32  # filters per CTA: 32 // kt warps
+# filters per CTA (CTA_FILTERS // kt warps); must match the library's build
+# (-DFSCNN_SF3_CTA_FILTERS, default 32 = two CTAs per SM, 64 = one)
+CTA_FILTERS = int(__import__("os").environ.get("FSCNN_SF3_CTA_FILTERS", "32"))
 SMEM_LIMIT = 227 * 1024
 
 
@@ -145,58 +147,23 @@ def _align(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-FLAT = -1  # sub-region "height" selecting the flat mode (sf_conv.cu: LY = 0)
 SMEM_2CTA = 113 * 1024  # per-CTA budget that keeps two CTAs resident per SM
 
 
-def flat_geometry(h: int, w: int):
-    """(tiles_h, tiles_w, box pitch, box rows) of the flat mode, or None when it does not
-    apply (mirrors flat_geometry in sf_conv.cu)."""
-    tw, th = math.ceil(w / TILE), math.ceil(h / TILE)
-    need = TILE * tw + 2
-    pitch = 36 if need <= 36 else (60 if need <= 60 else 0)
-    tpi = tw * th
-    if not pitch or not (tpi >= 32 or tpi == 16):
-        return None
-    ntr = min(th, (tw + 30) // tw + 1)
-    return th, tw, pitch, TILE * ntr + 2
-
-
-def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4, h: int = 0, w: int = 0,
-                     stages: int = STAGES) -> int:
+def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4, stages: int = STAGES) -> int:
     NWARP = CTA_FILTERS // kt
-    if ly == FLAT:
-        _, _, pitch, box_h = flat_geometry(h, w)
-        li, box = 2, _align(pitch * box_h * cc, 32)
-    else:
-        li, box = 8 // ly, _align(BOXW * (TILE * ly + 2) * cc, 32)
+    li, box = 8 // ly, _align(BOXW * (TILE * ly + 2) * cc, 32)
     n_chunks = math.ceil(c / cc)
     return (stages * li * box * 4 + stages * NWARP * ent_cap * 8 + 2 * stages * 8
             + NWARP * (n_chunks + 1) * 4)
 
 
-def pick_ly(h: int) -> int:
-    """Sub-region height 4*ly with the least padded rows (ties -> taller regions)."""
-    best = None
-    for ly in (8, 4, 2):
-        rows = math.ceil(h / (TILE * ly)) * TILE * ly
-        key = (rows, -ly)
-        if best is None or key < best[0]:
-            best = (key, ly)
-    return best[1]
-
-
-def pick_layout(n: int, h: int, w: int) -> int:
-    """Rectangular sub-region height (pick_ly), or FLAT when the flat mode idles clearly
-    fewer lanes (mirrors the auto rule of fscnn_sf_conv3x3_ex)."""
-    ly = pick_ly(h)
-    geo = flat_geometry(h, w)
-    if geo is None:
-        return ly
-    th, tw, _, _ = geo
-    rect = h * w / (math.ceil(h / (TILE * ly)) * TILE * ly * math.ceil(w / SUBW) * SUBW)
-    flat = n * h * w / (math.ceil(n * th * tw / 32) * 32 * 16)
-    return FLAT if flat > 1.03 * rect else ly
+def pick_ly(c: int, h: int) -> int:
+    """Sub-region height 4*ly (mirrors the auto rule of fscnn_sf_conv3x3_ex): 16x16
+    sub-regions measured fastest on every VGG16 width with 16-channel chunks (also at
+    56/28/14, where they pad more rows than 8x16); 8x16 for shallow inputs (c < 8) and
+    short images."""
+    return 2 if (c < 8 or h <= 8) else 4
 
 
 @dataclass
@@ -213,31 +180,32 @@ class PackedBank:
     nnz: int                   # nonzero weights
     _cache: dict = None
 
-    def chunk_plan(self, ly: int, h: int = 0, w: int = 0) -> tuple[int, int]:
-        """(cc, max_chunk_entries) for layout ly (FLAT needs h, w): the largest channel
-        chunk whose 2-stage ring keeps two CTAs per SM, else the largest that fits at all."""
-        key = (ly, h, w) if ly == FLAT else ly
+    def chunk_plan(self, ly: int) -> tuple[int, int]:
+        """(cc, max_chunk_entries) for sub-region height 4*ly: the largest channel chunk
+        whose 2-stage ring keeps two CTAs per SM (per-chunk ring coupling costs ~25% at 4
+        vs 8 channels, ~8% at 8 vs 16), else the largest that fits at all."""
         if self._cache is None:
             self._cache = {}
-        if key in self._cache:
-            return self._cache[key]
+        if ly in self._cache:
+            return self._cache[ly]
         import os
 
         forced = int(os.environ.get("FSCNN_SF3_CC", "0"))
         cands = []
-        for cc in ((forced,) if forced else (8, 4, 2, 1)):
-            if cc > self.c and cc != 1 and not forced:
+        sizes = sorted({16, 8, 4, 2, 1} | ({self.c} if self.c < 16 else set()), reverse=True)
+        for cc in ((forced,) if forced else sizes):
+            if cc > self.c and not forced:
                 continue
             n_chunks = math.ceil(self.c / cc)
             pad = n_chunks * cc - self.c
             cnt = np.pad(self.counts, ((0, 0), (0, pad)))
             mx = int(cnt.reshape(cnt.shape[0], n_chunks, cc).sum(axis=2).max())
             ent_cap = (mx + 4) & ~1
-            cands.append((cc, mx, sf3x3_smem_bytes(ly, cc, ent_cap, self.c, self.kt, h, w)))
-        for limit in (SMEM_2CTA, SMEM_LIMIT):
+            cands.append((cc, mx, sf3x3_smem_bytes(ly, cc, ent_cap, self.c, self.kt)))
+        for limit in ((SMEM_2CTA, SMEM_LIMIT) if CTA_FILTERS == 32 else (SMEM_LIMIT,)):
             for cc, mx, need in cands:
                 if need <= limit:
-                    self._cache[key] = (cc, mx)
+                    self._cache[ly] = (cc, mx)
                     return cc, mx
         raise RuntimeError("filter bank too dense for the fast kernel's shared memory")
 
@@ -313,9 +281,9 @@ def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, rel
     w = ldi - 1 if w is None else int(w)
     assert x.stride(3) == 1 and x.stride(1) == ldi * h and x.stride(0) == ldi * h * c
     assert c == bank.c and ldi >= w + 1
-    if ly == 0:
-        ly = pick_layout(n, h, w)
-    cc, mx = bank.chunk_plan(ly, h, w)
+    if ly <= 0:
+        ly = pick_ly(c, h)
+    cc, mx = bank.chunk_plan(ly)
     ho, wo = (h // 2, w // 2) if pool else (h, w)
     if out is None:
         out = halo_empty(n, bank.k, ho, wo, x.device)

@@ -81,9 +81,8 @@ class VGGEngine:
                 bias_t = torch.as_tensor(np.asarray(bias_np, np.float32) if not torch.is_tensor(bias_np) else bias_np)
                 bias_t = bias_t.to(dev, torch.float32).contiguous()
             bank = device.sf_pack(dense)
-            # ly = 0: the layout (sub-region height or flat mode) is picked per call for
-            # the actual batch size (device.pick_layout)
-            self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes, 0))
+            self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes,
+                                       device.pick_ly(c, h)))
             c = k
             if pool:
                 h //= 2

@@ -118,32 +118,17 @@ def test_multiply_count_matches_oracle(oracle):
 
 
 def test_launch_planner():
-    assert device.pick_ly(224) == 8 and device.pick_ly(112) == 4 and device.pick_ly(56) == 2
+    assert device.pick_ly(64, 224) == 4 and device.pick_ly(3, 224) == 2 and device.pick_ly(512, 14) == 4
     counts = np.full((16, 512), 5, np.int64)  # 16 groups x 512 channels, 4 nodes + sentinel
     bank = device.PackedBank(64, 512, 4, None, None, int(counts.sum()), counts, 0)
-    cc, mx = bank.chunk_plan(8)
-    assert cc == 8 and mx == 40
-    assert device.sf3x3_smem_bytes(8, cc, mx + 4, 512) <= device.SMEM_LIMIT
+    cc, mx = bank.chunk_plan(4)
+    assert cc == 16 and mx == 80  # 16-channel chunks keep two CTAs per SM
+    assert device.sf3x3_smem_bytes(4, cc, mx + 4, 512) <= device.SMEM_2CTA
+    shallow = device.PackedBank(64, 3, 4, None, None, 0, np.full((16, 3), 2, np.int64), 0)
+    assert shallow.chunk_plan(2) == (3, 6)  # one chunk holds all channels
     dense = device.PackedBank(64, 512, 4, None, None, 0, np.full((16, 512), 37, np.int64), 0)
     cc2, mx2 = dense.chunk_plan(2)  # a fully dense bank still fits (smaller chunks if needed)
     assert device.sf3x3_smem_bytes(2, cc2, mx2 + 4, 512) <= device.SMEM_LIMIT
-
-
-def test_flat_layout_planner():
-    # the flat mode takes the VGG16 widths the 16-wide sub-regions pad (56, 28)
-    assert device.flat_geometry(28, 28) == (7, 7, 36, 26)
-    assert device.flat_geometry(56, 56) == (14, 14, 60, 18)
-    assert device.flat_geometry(14, 14) == (4, 4, 36, 18)
-    assert device.flat_geometry(224, 224) is None and device.flat_geometry(8, 8) is None
-    assert device.pick_layout(32, 224, 224) == 8 and device.pick_layout(32, 112, 112) == 4
-    assert device.pick_layout(32, 56, 56) == device.FLAT and device.pick_layout(32, 28, 28) == device.FLAT
-    assert device.pick_layout(32, 14, 14) == device.pick_ly(14)  # partial tiles either way: no gain
-    # chunks shrink until a 2-stage ring fits two CTAs per SM
-    counts = np.full((16, 256), 5, np.int64)
-    bank = device.PackedBank(64, 256, 4, None, None, int(counts.sum()), counts, 0)
-    cc, mx = bank.chunk_plan(device.FLAT, 56, 56)
-    assert device.sf3x3_smem_bytes(device.FLAT, cc, (mx + 4) & ~1, 256, 4, 56, 56) <= device.SMEM_2CTA
-    assert cc == 4
 
 
 def test_workload_shapes_and_determinism():

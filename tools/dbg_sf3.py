@@ -10,7 +10,7 @@ xt, wt = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
 enc = device.encode_order(wt, "CHW")
 ref = device.sf_conv_exact(xt, enc.nodes, enc.seg_off, 64, 3, 3, 1, 1, None)
 bank = device.sf_pack(wt)
-print("bank total", bank.total, "nnz", bank.nnz, "plan", bank.chunk_plan(device.pick_ly(56)), flush=True)
+print("bank total", bank.total, "nnz", bank.nnz, "plan", bank.chunk_plan(device.pick_ly(bank.c, 56)), flush=True)
 for ly in (2, 4, 8):
     y = device.from_halo(device.sf_conv3x3(device.to_halo(xt), bank, None, relu=False, pool=False, w=56, ly=ly), 56)
     torch.cuda.synchronize()

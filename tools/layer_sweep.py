@@ -1,6 +1,7 @@
 """Time the fast sparse-filter kernel on all 13 VGG16 layer shapes (batch 32).
 
 usage: python tools/layer_sweep.py [ZERO_FRAC] [REPS]   -> one line per layer + total
+       SWEEP_LY=2|4|8 forces the sub-region height; SWEEP_LAYERS=1,5 selects layers
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,12 +11,15 @@ from paper_2212_08815_b200 import device, workloads as wl
 zf = float(sys.argv[1]) if len(sys.argv) > 1 else 0.9
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 tot_ms = tot_fl = 0.0
+only = os.environ.get("SWEEP_LAYERS")
 for li, (c, k, h, w) in enumerate(wl.vgg16_conv_shapes()):
+    if only and str(li) not in only.split(","):
+        continue
     x, wt, b = wl.sweep_layer(li, "sf", zf, n=32)
     bank = device.sf_pack(torch.from_numpy(wt).cuda())
     xh = device.to_halo(torch.from_numpy(x).cuda())
     bias = torch.from_numpy(b).cuda()
-    ly = device.pick_ly(h)
+    ly = int(os.environ.get("SWEEP_LY", "0")) or device.pick_ly(c, h)
     out = device.halo_empty(32, k, h, w)
     for _ in range(2):
         device.sf_conv3x3(xh, bank, bias, relu=True, pool=False, w=w, ly=ly, out=out)

@@ -14,7 +14,7 @@ x, wt, b = wl.sweep_layer(li, "sf", 0.9, n=32)
 bank = device.sf_pack(torch.from_numpy(wt).cuda())
 xh = device.to_halo(torch.from_numpy(x).cuda())
 bias = torch.from_numpy(b).cuda()
-ly = device.pick_ly(h)
+ly = device.pick_ly(c, h)
 print("layer", li, (c, k, h, w), "ly", ly, "plan", bank.chunk_plan(ly), flush=True)
 for _ in range(reps):
     y = device.sf_conv3x3(xh, bank, bias, relu=True, pool=False, w=w, ly=ly)
