@@ -50,13 +50,22 @@ def block(KT: int) -> str:
     NA = KT * 8                                              # acc pair operands
     A = lambda kl, py, h: f"%{kl * 8 + py * 2 + h}"          # acc pair
     P = lambda r, h: f"%{NA + r * 3 + h}"                    # patch pair
-    CUR, PP, CNT, CHS, RB = (f"%{NA + 18 + i}" for i in range(5))
+    # cursor, patch pointer and channel count arrive as plain inputs and are copied to
+    # block-local registers: with read-write ("+r") operands ptxas wrapped the whole
+    # dispatch loop in a per-nonzero convergence barrier (BSSY/BSYNC + an extra branch)
+    # whenever the cursor was not a simple induction variable of the caller's loop
+    I_CUR, I_PP, I_CNT, CHS, RB = (f"%{NA + 18 + i}" for i in range(5))
+    CUR, PP, CNT = "r_cur", "r_pp", "r_cnt"
     NC = KT * 9
     L = []
     e = L.append
     e("{")
     e(".reg .pred p_end;")
     e(".reg .b32 r_ix, r_i1, r_v1, r_a, r_b, r_c, r_d, r_e, r_f;")
+    e(".reg .b32 r_cur, r_pp, r_cnt;")
+    e(f"mov.b32 r_cur, {I_CUR};")
+    e(f"mov.b32 r_pp, {I_PP};")
+    e(f"mov.b32 r_cnt, {I_CNT};")
     e(".reg .f32 f_v;")
     e(".reg .b64 d_vv;")
     # targets: 0..NC-1 entry, NC..2NC-1 channel-last entry, 2NC empty channel
@@ -147,9 +156,8 @@ def emit(KT: int) -> None:
     print("    unsigned long long pt2[6][3];")
     print(f'    asm volatile("{block(KT)}"')
     print(f"                 : {outs},")
-    print(f"                   {pts},")
-    print('                   "+r"(cur), "+r"(patch), "+r"(n_ch)')
-    print('                 : "r"(ch_bytes), "n"(ROW_BYTES)')
+    print(f"                   {pts}")
+    print('                 : "r"(cur), "r"(patch), "r"(n_ch), "r"(ch_bytes), "n"(ROW_BYTES)')
     print('                 : "memory");')
     print("}")
     print()

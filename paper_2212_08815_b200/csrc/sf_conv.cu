@@ -91,6 +91,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// The value of lane 0 through redux.sync, which ptxas knows to be warp-uniform (it lands
+// in a uniform register).  Used for the entry cursor: when ptxas cannot prove the jump
+// index uniform it guards the jump-table loop with a per-nonzero convergence barrier
+// (BSSY/BSYNC + an extra branch per nonzero).
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) {
+    uint32_t r;
+    asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -152,7 +162,8 @@ struct Sf3Params {
     int relu;
     int pool;                 // fused 2x2 max-pool
     int stages;               // ring depth (<= MAX_STAGES)
-    int dbg;                  // debug: 1 = skip compute, 3 = no TMA, 4 = no bulk copies (1,3,4 skip compute)
+    int dbg;                  // debug (FSCNN_SF3_DEBUG, wrong results): 5 = no box TMA;
+                              // 7 = entries restaged per warp, boxes never restaged
 };
 
 template <int LY, int KT>
@@ -207,14 +218,14 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
 #pragma unroll
     for (int li = 0; li < LI; ++li) n_box += (sub0 + li < p.n_sub);
     const uint32_t box_bytes =
-        (p.dbg == 3) ? 0u : (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
+        p.dbg == 5 ? 0u : (uint32_t)n_box * (uint32_t)(BOXW * BOXH * p.cc * 4);
 
     // Each warp stages its own entry run for chunk ch (lane 0); dead groups arrive empty.
     auto refill_entries = [&](int ch) {
         const int s = ch % STAGES;
         uint32_t nb = 0;
         int lo = 0;
-        if (live && p.dbg != 4) {
+        if (live) {
             const int a = cofs[warp * (n_chunks + 1) + ch];
             const int b = cofs[warp * (n_chunks + 1) + ch + 1];
             lo = a & ~1;  // 16-byte aligned start
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     auto refill_boxes = [&](int ch) {
         const int s = ch % STAGES;
         mbar_expect_tx(&full[s], box_bytes);
-        if (p.dbg == 3) return;
+        if (p.dbg == 5) return;
 #pragma unroll
         for (int li = 0; li < LI; ++li) {
             int sub = sub0 + li;
@@ -244,6 +255,11 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
         }
     };
 
+    // A dead group (k not a multiple of the CTA's filters) walks "empty channel"
+    // markers, so the dispatch call needs no enclosing branch.
+    if (!live)
+        for (int i = lane; i < STAGES * p.ent_cap; i += 32)
+            ent_s[((i / p.ent_cap) * NWARP + warp) * p.ent_cap + i % p.ent_cap] = make_int2(2 * KT * 9, 0);
     if (lane == 0)
         for (int ch = 0; ch < STAGES && ch < n_chunks; ++ch) {
             refill_entries(ch);
@@ -269,11 +285,12 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
         __syncwarp();
         const int c0 = ch * p.cc;
         const int cnt = min(p.cc, p.c - c0);
-        if (live && p.dbg == 0) {
+        {
             const int2 *ents = ent_s + (s * NWARP + warp) * p.ent_cap;
-            const int e0 = cofs[warp * (n_chunks + 1) + ch] & 1;  // offset inside aligned copy
+            // offset inside the 16-byte aligned copy
+            const int e0 = live ? cofs[warp * (n_chunks + 1) + ch] & 1 : 0;
             const float *box = in_s + s * stage_in_floats + li * p.box_floats;
-            sf3x3_chunk<BOXW * 4>(acc2, smem_u32(ents + e0),
+            sf3x3_chunk<BOXW * 4>(acc2, warp_uniform(smem_u32(ents + e0)),
                                   smem_u32(box + (TILE * ly) * BOXW + TILE * lx), cnt,
                                   (uint32_t)(BOXH * BOXW * 4));
         }
@@ -283,7 +300,14 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
         if (lane == 0 && ch + STAGES < n_chunks) {
             refill_entries(ch + STAGES);
             // the counter only grows: every NWARP-th arrival closes a round
-            if ((atomicAdd(&done[s], 1) + 1) % NWARP == 0) refill_boxes(ch + STAGES);
+            const int prev = atomicAdd(&done[s], 1);
+            if (p.dbg == 7) {
+                // debug: boxes are never restaged (stale input) and the first warp to
+                // leave does the box arrival -- measures the cost of the warp coupling
+                if (prev % NWARP == 0) mbar_expect_tx(&full[s], 0);
+            } else if ((prev + 1) % NWARP == 0) {
+                refill_boxes(ch + STAGES);
+            }
         }
         __syncwarp();
     }

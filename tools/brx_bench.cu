@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(512, 1) bench(const int2 *ents_g, int n_ent, i
         uint32_t end = cur + n_ent * 8;
         // current protocol: one call = one chunk of 8 channels, each (per) entries + sentinel slot
 #pragma unroll 1
-        for (int q = 0; q < 8; ++q) { sf3x3_chunk<34 * 20 * 4>(acc2, cur + 8u * starts[q], pbase, 8); }
+        for (int q = 0; q < 8; ++q) { sf3x3_chunk<20 * 4>(acc2, cur + 8u * starts[q], pbase, 8, 34 * 20 * 4); }
         (void)end;
     }
     long long t1 = clock64();
