@@ -154,6 +154,7 @@ struct Sf3Params {
     int ldo;                  // output row pitch (floats)
     int tiles_h, tiles_w;     // sub-region grid per image
     int n_sub;                // n * tiles_h * tiles_w
+    int n_fb;                 // filter blocks (CTA_FILTERS filters each)
     int cc;                   // channels per chunk
     int ent_cap;              // entry slots per warp per stage (int2)
     int box_floats;           // floats per sub-region box per stage
@@ -184,8 +185,11 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     int *cofs = done + 2 * STAGES;                           // [NWARP][n_chunks + 1] run starts
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub0 = blockIdx.x * LI;
-    const int g0 = blockIdx.y * NWARP;
+    // 1-D grid, filter block fastest: the CTAs of one spatial unit (all filter blocks)
+    // run together, so its input boxes are read from DRAM once and then hit in L2
+    const int n_fb = p.n_fb;
+    const int sub0 = (int)(blockIdx.x / n_fb) * LI;
+    const int g0 = (int)(blockIdx.x % n_fb) * NWARP;
     const int n_groups = (p.k + KT - 1) / KT;
     const int n_chunks = (p.c + p.cc - 1) / p.cc;
 
@@ -429,7 +433,13 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
         return FSCNN_ERR_CUDA;
     }
     int n_groups = (int)ceil_div(p.k, KT);
-    dim3 grid((unsigned)ceil_div(p.n_sub, LI), (unsigned)ceil_div(n_groups, NWARP));
+    p.n_fb = (int)ceil_div(n_groups, NWARP);
+    const int64_t n_cta = ceil_div(p.n_sub, LI) * (int64_t)p.n_fb;
+    if (n_cta > 0x7fffffff) {
+        set_error("sf3x3: grid of %lld CTAs too large", (long long)n_cta);
+        return FSCNN_ERR_UNSUPPORTED;
+    }
+    dim3 grid((unsigned)n_cta, 1, 1);
     kern<<<grid, NTHREADS, smem, st>>>(map, p);
     return check_launch("sf3x3_kernel");
 }
