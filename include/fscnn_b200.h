@@ -87,6 +87,37 @@ int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
                  int64_t mid, int64_t inner, float *dst, int64_t d_b, int64_t d_o, int64_t d_m,
                  int64_t d_i, void *stream);
 
+/* Node-preserving variants: decode also writes a presence mask (1 byte per element,
+ * same element offsets as dst), and the masked encoder stores an entry iff its mask
+ * byte is set, whatever its value.  decode -> masked encode in another axis order is
+ * transpose_matrix / transpose_tensor3 (kernels.py:360-411): values, including explicit
+ * zero-valued nodes, move untouched. */
+int fscnn_decode_masked(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
+                        int64_t outer, int64_t mid, int64_t inner, float *dst, uint8_t *mask,
+                        int64_t d_b, int64_t d_o, int64_t d_m, int64_t d_i, void *stream);
+int fscnn_encode_masked_offsets(const float *src, const uint8_t *mask, int64_t batch,
+                                int64_t outer, int64_t mid, int64_t inner, int64_t s_b,
+                                int64_t s_o, int64_t s_m, int64_t s_i, int64_t *seg_off,
+                                int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                                void *stream);
+int fscnn_encode_masked_nodes(const float *src, const uint8_t *mask, int64_t batch,
+                              int64_t outer, int64_t mid, int64_t inner, int64_t s_b, int64_t s_o,
+                              int64_t s_m, int64_t s_i, const int64_t *seg_off, fscnn_node *nodes,
+                              int64_t *matrix_off, int64_t *tensor_off, void *stream);
+
+/* Segment gather (node-format restructuring, e.g. pad_tensor on CHW nodes,
+ * layers.py:521-535): new segment j is a verbatim copy of old segment map[j] (nodes and
+ * sentinel; explicit zero-valued nodes survive) or, for map[j] < 0, an empty segment.
+ * Two passes like the encoder: offsets (+ total, workspace as fscnn_encode_*), then
+ * nodes.  old_total = length of the old node buffer. */
+int fscnn_remap_segments_offsets(const int64_t *old_seg_off, int64_t n_old, int64_t old_total,
+                                 const int64_t *map, int64_t n_new, int64_t *new_seg_off,
+                                 int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                                 void *stream);
+int fscnn_remap_segments_nodes(const fscnn_node *old_nodes, const int64_t *old_seg_off,
+                               int64_t n_old, int64_t old_total, const int64_t *map, int64_t n_new,
+                               const int64_t *new_seg_off, fscnn_node *new_nodes, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Sparse-Filter convolution, reference order (bit-exact).
  * Replaces _conv_all_filters_kernel (layers.py:170-180) / _conv_filter_sparse_kernel
@@ -100,6 +131,14 @@ int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
 int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_node *nodes,
                         const int64_t *seg_off, int k, int h_f, int w_f, int stride, int pad,
                         const float *bias, int relu, float *y, void *stream);
+
+/* Dense baseline convolution (bit-exact): conv_forward_dense (layers.py:326-342) over
+ * _dense_conv_kernel (kernels.py:169-192) -- taps kh outer, kw inner, channels
+ * ascending, every weight multiplied (zeros too, so NaN/Inf inputs propagate as in the
+ * reference), then + bias[k].  wt: dense [K][C][h_f][w_f]; x, y as above. */
+int fscnn_dense_conv_exact(const float *x, int n, int c, int h, int w, const float *wt, int k,
+                           int h_f, int w_f, int stride, int pad, const float *bias, float *y,
+                           void *stream);
 
 /* ---------------------------------------------------------------------------
  * Sparse-Filter convolution, fast path (3x3, stride 1, pad 1 -- every VGG16 conv).
@@ -170,6 +209,18 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
  *   Layout converters between the reference's (W,H,C) DenseTensor3 memory and NCHW.
  * ------------------------------------------------------------------------- */
 int fscnn_relu(const float *x, int64_t count, float *y, void *stream);
+/* kind 0 = fscnn_relu; 1 = leaky ReLU np.where(x > 0, x, slope*x) (layers.py:484);
+ * 2 = the node-format ReLU keep rule x > 0 ? x : 0 (layers.py:488-489, with
+ * rebuild_tensor3 sparse_core.py:460-473 done by decode -> this -> re-encode). */
+int fscnn_activation(const float *x, int64_t count, int kind, float slope, float *y,
+                     void *stream);
+/* apply_batchnorm (layers.py:507-509) on NCHW: ((x - mean) / sqrt(var + eps)) * scale + shift
+ * with numpy's float32 op order (bit-exact). */
+int fscnn_batchnorm(const float *x, int n, int c, int h, int w, const float *scale,
+                    const float *shift, const float *mean, const float *var, float eps, float *y,
+                    void *stream);
+/* pad_tensor (layers.py:513-520) on NCHW: y is (h + 2p) x (w + 2p), zeros around. */
+int fscnn_pad2d(const float *x, int n, int c, int h, int w, int p, float *y, void *stream);
 int fscnn_pool2d(const float *x, int n, int c, int h, int w, int h_p, int w_p, int use_max,
                  float *y, void *stream);
 int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_nchw,

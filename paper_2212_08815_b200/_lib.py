@@ -33,6 +33,11 @@ _SIGNATURES = {
     "fscnn_encode_offsets": (_i32, [_vp] + [_i64] * 8 + [_vp, _vp, _vp, _sz, _vp]),
     "fscnn_encode_nodes": (_i32, [_vp] + [_i64] * 8 + [_vp, _vp, _vp, _vp, _vp]),
     "fscnn_decode": (_i32, [_vp, _vp] + [_i64] * 4 + [_vp] + [_i64] * 4 + [_vp]),
+    "fscnn_decode_masked": (_i32, [_vp, _vp] + [_i64] * 4 + [_vp, _vp] + [_i64] * 4 + [_vp]),
+    "fscnn_encode_masked_offsets": (_i32, [_vp, _vp] + [_i64] * 8 + [_vp, _vp, _vp, _sz, _vp]),
+    "fscnn_encode_masked_nodes": (_i32, [_vp, _vp] + [_i64] * 8 + [_vp, _vp, _vp, _vp, _vp]),
+    "fscnn_remap_segments_offsets": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "fscnn_remap_segments_nodes": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "fscnn_sf_conv_exact": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "fscnn_sf_pack_kt": (_i32, []),
     "fscnn_sf_pack_offsets": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
@@ -42,7 +47,11 @@ _SIGNATURES = {
     "fscnn_kcrs_to_crsk": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_si_pack3x3": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fscnn_si_conv3x3": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
+    "fscnn_dense_conv_exact": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fscnn_relu": (_i32, [_vp, _i64, _vp, _vp]),
+    "fscnn_activation": (_i32, [_vp, _i64, _i32, ctypes.c_float, _vp, _vp]),
+    "fscnn_batchnorm": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, ctypes.c_float, _vp, _vp]),
+    "fscnn_pad2d": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_pool2d": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_whc_to_nchw": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_nchw_to_whc": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),

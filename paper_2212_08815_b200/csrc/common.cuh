@@ -44,4 +44,12 @@ __device__ __forceinline__ float relu_np(float v) {
     return __int_as_float(keep ? u : 0);
 }
 
+// x86 float arithmetic with one NaN operand returns that operand, quieted; CUDA returns
+// the canonical NaN.  Elementwise ops that must match numpy bit-for-bit (node payloads
+// are compared as raw bytes) route NaNs through here.
+__device__ __forceinline__ bool is_nan_bits(float v) {
+    return (__float_as_int(v) & 0x7fffffff) > 0x7f800000;
+}
+__device__ __forceinline__ float nan_quiet(float v) { return __int_as_float(__float_as_int(v) | 0x00400000); }
+
 }  // namespace fscnn

@@ -1,5 +1,9 @@
 // Memory-bound layers between convolutions and layout converters.
 //   relu      -- np.maximum(x, 0) (layers.py:469-484)
+//   act       -- leaky ReLU np.where(x > 0, x, s*x) (layers.py:484) and the node-format
+//                ReLU keep rule x > 0 (layers.py:488-489: NaN and -0.0 dropped)
+//   batchnorm -- ((x - mean) / sqrt(var + eps)) * scale + shift (layers.py:507-509)
+//   pad2d     -- zero padding of the spatial extents (layers.py:513-520)
 //   pool2d    -- _pool_dense_kernel (layers.py:250-271) on NCHW
 //   whc<->nchw -- DenseTensor3 memory (sparse_core.py:9-13) <-> device NCHW
 //   kcrs->crsk -- dense filter bank transposed for the sparse-input kernel
@@ -31,6 +35,53 @@ __global__ void relu_kernel(const float *__restrict__ x, int64_t n, float *__res
     for (int64_t i = head + t0; i < n; i += stride) y[i] = relu_np(x[i]);
 }
 
+// kind 1: leaky ReLU (x > 0 ? x : slope * x, one fp32 multiply like numpy);
+// kind 2: the node-format ReLU keep rule, x > 0 ? x : 0 (NaN -> 0, -0.0 -> 0, so the
+// re-encode drops exactly the nodes the reference drops).
+__global__ void act_kernel(const float *__restrict__ x, int64_t n, int kind, float slope,
+                           float *__restrict__ y) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        float v = x[i];
+        if (kind == 1 && is_nan_bits(v)) y[i] = nan_quiet(v);  // numpy keeps the payload
+        else y[i] = v > 0.0f ? v : (kind == 1 ? __fmul_rn(slope, v) : 0.0f);
+    }
+}
+
+// NCHW, per-channel statistics; numpy's float32 op order, no contraction.
+__global__ void batchnorm_kernel(const float *__restrict__ x, int64_t total, int c_n, int64_t hw,
+                                 const float *__restrict__ scale, const float *__restrict__ shift,
+                                 const float *__restrict__ mean, const float *__restrict__ var,
+                                 float eps, float *__restrict__ y) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+        int c = (int)((i / hw) % c_n);
+        const float xv = x[i];
+        if (is_nan_bits(xv)) {  // numpy: the NaN operand propagates, quieted
+            y[i] = nan_quiet(xv);
+            continue;
+        }
+        float sd = __fsqrt_rn(__fadd_rn(var[c], eps));
+        float v = __fdiv_rn(__fsub_rn(xv, mean[c]), sd);
+        y[i] = __fadd_rn(__fmul_rn(v, scale[c]), shift[c]);
+    }
+}
+
+// NCHW (h, w) -> (h + 2p, w + 2p) with zeros around; one thread per output element.
+__global__ void pad2d_kernel(const float *__restrict__ x, int64_t total, int h, int w, int p,
+                             float *__restrict__ y) {
+    const int ho = h + 2 * p, wo = w + 2 * p;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        int xo = (int)(t % wo);
+        int64_t r = t / wo;
+        int yo = (int)(r % ho);
+        int64_t nc = r / ho;
+        int xi = xo - p, yi = yo - p;
+        y[t] = (xi >= 0 && xi < w && yi >= 0 && yi < h) ? x[(nc * h + yi) * (int64_t)w + xi] : 0.0f;
+    }
+}
+
 // One thread per output element (n, c, ho, wo); reads the window rows (ph outer, pw inner).
 __global__ void pool2d_kernel(const float *__restrict__ x, int64_t total, int h, int w, int h_p,
                               int w_p, int use_max, float *__restrict__ y) {
@@ -49,11 +100,11 @@ __global__ void pool2d_kernel(const float *__restrict__ x, int64_t total, int h,
                 float v = src[(int64_t)ph * w + pw];
                 if (use_max) {
                     if (v > acc) acc = v;
-                } else {
-                    acc = __fadd_rn(acc, v);
+                } else if (!is_nan_bits(acc)) {  // numpy: the first NaN summed wins
+                    acc = is_nan_bits(v) ? nan_quiet(v) : __fadd_rn(acc, v);
                 }
             }
-        y[t] = use_max ? acc : __fdiv_rn(acc, area);
+        y[t] = use_max ? acc : (is_nan_bits(acc) ? acc : __fdiv_rn(acc, area));
     }
 }
 
@@ -154,6 +205,41 @@ int fscnn_relu(const float *x, int64_t count, float *y, void *stream) {
     else
         relu_kernel<false><<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(x, count, y);
     FSCNN_LAUNCH_CHECK("relu_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_activation(const float *x, int64_t count, int kind, float slope, float *y,
+                     void *stream) {
+    FSCNN_REQUIRE(count >= 0 && (count == 0 || (x && y)), "bad activation arguments");
+    FSCNN_REQUIRE(kind >= 0 && kind <= 2, "unknown activation kind");
+    if (kind == 0) return fscnn_relu(x, count, y, stream);
+    if (count == 0) return FSCNN_OK;
+    act_kernel<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(x, count, kind, slope, y);
+    FSCNN_LAUNCH_CHECK("act_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_batchnorm(const float *x, int n, int c, int h, int w, const float *scale,
+                    const float *shift, const float *mean, const float *var, float eps, float *y,
+                    void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    int64_t total = (int64_t)n * c * h * w;
+    if (total == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && y && scale && shift && mean && var, "null buffer");
+    batchnorm_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+        x, total, c, (int64_t)h * w, scale, shift, mean, var, eps, y);
+    FSCNN_LAUNCH_CHECK("batchnorm_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_pad2d(const float *x, int n, int c, int h, int w, int p, float *y, void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    FSCNN_REQUIRE(p >= 0, "pad width must be non-negative");
+    int64_t total = (int64_t)n * c * (h + 2 * p) * (w + 2 * p);
+    if (total == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(y && (x || (int64_t)n * c * h * w == 0), "null buffer");
+    pad2d_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(x, total, h, w, p, y);
+    FSCNN_LAUNCH_CHECK("pad2d_kernel");
     return FSCNN_OK;
 }
 

@@ -36,6 +36,28 @@ struct StridedSrc {
         return {p + b * s_b + o * s_o + m * s_m};
     }
     __device__ __forceinline__ float at(Fiber f, int64_t i) const { return f.p[i * s_i]; }
+    __device__ __forceinline__ bool present(Fiber f, int64_t i) const { return at(f, i) != 0.0f; }
+};
+
+// A strided value view plus a presence mask with the same element offsets: an entry is
+// stored iff its mask byte is set, whatever its value (node-preserving transposes keep
+// explicit zero-valued nodes this way).
+struct MaskedSrc {
+    const float *p;
+    const uint8_t *m;
+    int64_t outer, mid, inner, s_b, s_o, s_m, s_i;
+    struct Fiber {
+        const float *p;
+        const uint8_t *m;
+    };
+    __device__ __forceinline__ Fiber fiber(int64_t s) const {
+        int64_t mm = s % mid;
+        int64_t bo = s / mid;
+        int64_t off = (bo / outer) * s_b + (bo % outer) * s_o + mm * s_m;
+        return {p + off, m + off};
+    }
+    __device__ __forceinline__ float at(Fiber f, int64_t i) const { return f.p[i * s_i]; }
+    __device__ __forceinline__ bool present(Fiber f, int64_t i) const { return f.m[i * s_i] != 0; }
 };
 
 // Fast-path filter packing: segment s = g*C + c; inner i = kl*9 + tap reads
@@ -57,6 +79,7 @@ struct SfPackSrc {
         int64_t kl = i / 9, tap = i - kl * 9;
         return kl < f.kmax ? f.p[kl * c * 9 + tap] : 0.0f;
     }
+    __device__ __forceinline__ bool present(Fiber f, int64_t i) const { return at(f, i) != 0.0f; }
 };
 
 template <class Src>
@@ -65,7 +88,7 @@ __global__ void count_thread_kernel(Src src, int64_t n_seg, int64_t *cnt) {
     if (s >= n_seg) return;
     auto b = src.fiber(s);
     int64_t n = 0;
-    for (int64_t i = 0; i < src.inner; ++i) n += (src.at(b, i) != 0.0f);
+    for (int64_t i = 0; i < src.inner; ++i) n += src.present(b, i);
     cnt[s] = n + 1;
 }
 
@@ -78,7 +101,7 @@ __global__ void count_warp_kernel(Src src, int64_t n_seg, int64_t *cnt) {
     int64_t n = 0;
     for (int64_t i0 = 0; i0 < src.inner; i0 += 32) {
         int64_t i = i0 + lane;
-        bool nz = (i < src.inner) && (src.at(b, i) != 0.0f);
+        bool nz = (i < src.inner) && src.present(b, i);
         n += __popc(__ballot_sync(0xffffffffu, nz));
     }
     if (lane == 0) cnt[s] = n + 1;
@@ -91,10 +114,8 @@ __global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_o
     if (s >= n_seg) return;
     auto b = src.fiber(s);
     int64_t p = seg_off[s];
-    for (int64_t i = 0; i < src.inner; ++i) {
-        float v = src.at(b, i);
-        if (v != 0.0f) nodes[p++] = make_int2((int)i, __float_as_int(v));
-    }
+    for (int64_t i = 0; i < src.inner; ++i)
+        if (src.present(b, i)) nodes[p++] = make_int2((int)i, __float_as_int(src.at(b, i)));
     nodes[p] = make_int2(sentinel, 0);
 }
 
@@ -109,8 +130,8 @@ __global__ void write_warp_kernel(Src src, int64_t n_seg, const int64_t *seg_off
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t i0 = 0; i0 < src.inner; i0 += 32) {
         int64_t i = i0 + lane;
-        float v = (i < src.inner) ? src.at(b, i) : 0.0f;
-        bool nz = v != 0.0f;
+        bool nz = (i < src.inner) && src.present(b, i);
+        float v = nz ? src.at(b, i) : 0.0f;
         unsigned m = __ballot_sync(0xffffffffu, nz);
         if (nz) nodes[p + __popc(m & lt)] = make_int2((int)i, __float_as_int(v));
         p += __popc(m);
@@ -258,23 +279,62 @@ int encode_nodes_impl(const Src &src, int64_t n_seg, bool warp_mode, const int64
 
 // --- decoder ----------------------------------------------------------------------
 
+// mask (optional, same element offsets as dst) receives 1 where a node is stored
 __global__ void decode_kernel(const int2 *nodes, const int64_t *seg_off, int64_t n_seg,
-                              int64_t outer, int64_t mid, int64_t inner, float *dst, int64_t d_b,
-                              int64_t d_o, int64_t d_m, int64_t d_i) {
+                              int64_t outer, int64_t mid, int64_t inner, float *dst, uint8_t *mask,
+                              int64_t d_b, int64_t d_o, int64_t d_m, int64_t d_i) {
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= n_seg) return;
     int64_t m = s % mid, bo = s / mid, o = bo % outer, b = bo / outer;
-    float *d = dst + b * d_b + o * d_o + m * d_m;
+    const int64_t off = b * d_b + o * d_o + m * d_m;
+    float *d = dst + off;
     int64_t p = seg_off[s];
     int2 nd = nodes[p];
     for (int64_t i = 0; i < inner; ++i) {
         float v = 0.0f;
-        if (nd.x == i) {
+        const bool hit = nd.x == i;
+        if (hit) {
             v = __int_as_float(nd.y);
             nd = nodes[++p];
         }
         d[i * d_i] = v;
+        if (mask) mask[off + i * d_i] = hit;
     }
+}
+
+// --- segment gather ------------------------------------------------------------------
+// New segment j is a copy of old segment map[j] (its nodes and sentinel, values and
+// indices untouched -- explicit zero-valued nodes survive), or empty (sentinel only)
+// when map[j] < 0.  pad_tensor on CHW nodes (layers.py:521-535) is this gather.
+
+__device__ __forceinline__ int64_t old_seg_len(const int64_t *off, int64_t n, int64_t total, int64_t s) {
+    return ((s + 1 < n) ? off[s + 1] : total) - off[s];
+}
+
+__global__ void remap_count_kernel(const int64_t *old_off, int64_t n_old, int64_t old_total,
+                                   const int64_t *map, int64_t n_new, int64_t *cnt) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n_new) return;
+    int64_t s = map[j];
+    cnt[j] = s < 0 ? 1 : old_seg_len(old_off, n_old, old_total, s);
+}
+
+// one warp per new segment, lanes copy the run
+__global__ void remap_copy_kernel(const int2 *old_nodes, const int64_t *old_off, int64_t n_old,
+                                  int64_t old_total, const int64_t *map, int64_t n_new,
+                                  const int64_t *new_off, int2 *new_nodes) {
+    int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (j >= n_new) return;
+    int64_t s = map[j];
+    int2 *dst = new_nodes + new_off[j];
+    if (s < 0) {
+        if (lane == 0) dst[0] = make_int2(-1, 0);
+        return;
+    }
+    const int2 *src = old_nodes + old_off[s];
+    int64_t len = old_seg_len(old_off, n_old, old_total, s);
+    for (int64_t i = lane; i < len; i += 32) dst[i] = src[i];
 }
 
 constexpr int kSfPackKt = 4;  // default filters per group (sf_conv.cu supports 4 and 8)
@@ -346,9 +406,89 @@ int fscnn_decode(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
     if (n_seg == 0 || inner == 0) return FSCNN_OK;
     FSCNN_REQUIRE(nodes && seg_off && dst, "null buffer");
     decode_kernel<<<(unsigned)ceil_div(n_seg, 128), 128, 0, as_stream(stream)>>>(
-        reinterpret_cast<const int2 *>(nodes), seg_off, n_seg, outer, mid, inner, dst, d_b, d_o,
-        d_m, d_i);
+        reinterpret_cast<const int2 *>(nodes), seg_off, n_seg, outer, mid, inner, dst, nullptr, d_b,
+        d_o, d_m, d_i);
     FSCNN_LAUNCH_CHECK("decode_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_decode_masked(const fscnn_node *nodes, const int64_t *seg_off, int64_t batch,
+                        int64_t outer, int64_t mid, int64_t inner, float *dst, uint8_t *mask,
+                        int64_t d_b, int64_t d_o, int64_t d_m, int64_t d_i, void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    int64_t n_seg = batch * outer * mid;
+    if (n_seg == 0 || inner == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(nodes && seg_off && dst && mask, "null buffer");
+    decode_kernel<<<(unsigned)ceil_div(n_seg, 128), 128, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2 *>(nodes), seg_off, n_seg, outer, mid, inner, dst, mask, d_b,
+        d_o, d_m, d_i);
+    FSCNN_LAUNCH_CHECK("decode_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_encode_masked_offsets(const float *src, const uint8_t *mask, int64_t batch,
+                                int64_t outer, int64_t mid, int64_t inner, int64_t s_b,
+                                int64_t s_o, int64_t s_m, int64_t s_i, int64_t *seg_off,
+                                int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    FSCNN_REQUIRE(total_nodes != nullptr, "total_nodes is NULL");
+    int64_t n_seg = batch * outer * mid;
+    FSCNN_REQUIRE(n_seg == 0 || ((src && mask) || inner == 0) && seg_off != nullptr, "null buffer");
+    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i};
+    return encode_offsets_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, total_nodes,
+                               workspace, workspace_bytes, as_stream(stream));
+}
+
+int fscnn_encode_masked_nodes(const float *src, const uint8_t *mask, int64_t batch,
+                              int64_t outer, int64_t mid, int64_t inner, int64_t s_b, int64_t s_o,
+                              int64_t s_m, int64_t s_i, const int64_t *seg_off, fscnn_node *nodes,
+                              int64_t *matrix_off, int64_t *tensor_off, void *stream) {
+    FSCNN_REQUIRE(batch >= 0 && outer >= 0 && mid >= 0 && inner >= 0, "negative extent");
+    int64_t n_seg = batch * outer * mid;
+    if (n_seg == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(seg_off != nullptr && nodes != nullptr, "null buffer");
+    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i};
+    cudaStream_t st = as_stream(stream);
+    int rc = encode_nodes_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, nodes, st);
+    if (rc != FSCNN_OK) return rc;
+    if (matrix_off || tensor_off) {
+        side_tables_kernel<<<(unsigned)ceil_div(n_seg, 256), 256, 0, st>>>(
+            seg_off, n_seg, mid, outer * mid, matrix_off, tensor_off);
+        FSCNN_LAUNCH_CHECK("side_tables_kernel");
+    }
+    return FSCNN_OK;
+}
+
+int fscnn_remap_segments_offsets(const int64_t *old_seg_off, int64_t n_old, int64_t old_total,
+                                 const int64_t *map, int64_t n_new, int64_t *new_seg_off,
+                                 int64_t *total_nodes, void *workspace, size_t workspace_bytes,
+                                 void *stream) {
+    FSCNN_REQUIRE(n_old >= 0 && n_new >= 0 && old_total >= 0, "negative extent");
+    FSCNN_REQUIRE(total_nodes != nullptr, "total_nodes is NULL");
+    cudaStream_t st = as_stream(stream);
+    if (n_new == 0) {
+        cudaMemsetAsync(total_nodes, 0, sizeof(int64_t), st);
+        return check_launch("memset total");
+    }
+    FSCNN_REQUIRE(map && new_seg_off && (n_old == 0 || old_seg_off), "null buffer");
+    remap_count_kernel<<<(unsigned)ceil_div(n_new, 256), 256, 0, st>>>(old_seg_off, n_old, old_total,
+                                                                       map, n_new, new_seg_off);
+    FSCNN_LAUNCH_CHECK("remap_count_kernel");
+    return scan_inplace(new_seg_off, n_new, total_nodes, workspace, workspace_bytes, st);
+}
+
+int fscnn_remap_segments_nodes(const fscnn_node *old_nodes, const int64_t *old_seg_off,
+                               int64_t n_old, int64_t old_total, const int64_t *map, int64_t n_new,
+                               const int64_t *new_seg_off, fscnn_node *new_nodes, void *stream) {
+    FSCNN_REQUIRE(n_old >= 0 && n_new >= 0 && old_total >= 0, "negative extent");
+    if (n_new == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(map && new_seg_off && new_nodes && (n_old == 0 || (old_nodes && old_seg_off)),
+                  "null buffer");
+    remap_copy_kernel<<<(unsigned)ceil_div(n_new * 32, 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const int2 *>(old_nodes), old_seg_off, n_old, old_total, map, n_new,
+        new_seg_off, reinterpret_cast<int2 *>(new_nodes));
+    FSCNN_LAUNCH_CHECK("remap_copy_kernel");
     return FSCNN_OK;
 }
 

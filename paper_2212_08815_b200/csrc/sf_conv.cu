@@ -67,6 +67,38 @@ __global__ void sf_exact_kernel(const float *__restrict__ x, int c_n, int h_i, i
     y[(((int64_t)img * k_n + k) * n_h + i) * n_w + j] = v;
 }
 
+// Dense baseline conv (conv_forward_dense, layers.py:326-342, over _dense_conv_kernel
+// kernels.py:169-192): taps kh outer, kw inner, channels ascending, every weight
+// (zeros included) multiplied as inp * filt, then + bias -- bit-exact with numba.
+// Same thread mapping as sf_exact_kernel; wt is the dense [K][C][h_f][w_f] bank.
+__global__ void dense_exact_kernel(const float *__restrict__ x, int c_n, int h_i, int w_i,
+                                   const float *__restrict__ wt, int k_n, int h_f, int w_f,
+                                   int stride, int pad, int n_h, int n_w,
+                                   const float *__restrict__ bias, float *__restrict__ y) {
+    int k = blockIdx.y;
+    int img = blockIdx.z;
+    int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= n_h * n_w) return;
+    int i = pix / n_w, j = pix % n_w;
+    const int64_t plane = (int64_t)h_i * w_i;
+    const float *xi = x + (int64_t)img * c_n * plane;
+    const float *wk = wt + (int64_t)k * c_n * h_f * w_f;
+    float acc = 0.0f;
+    for (int kk = 0; kk < h_f; ++kk) {
+        int h_in = kk + i * stride - pad;
+        if (h_in < 0 || h_in >= h_i) continue;
+        for (int l = 0; l < w_f; ++l) {
+            int w_in = l + j * stride - pad;
+            if (w_in < 0 || w_in >= w_i) continue;
+            const float *px = xi + (int64_t)h_in * w_i + w_in;
+            const float *pw = wk + kk * w_f + l;
+            for (int c = 0; c < c_n; ++c)
+                acc = __fadd_rn(acc, __fmul_rn(px[c * plane], pw[(int64_t)c * h_f * w_f]));
+        }
+    }
+    y[(((int64_t)img * k_n + k) * n_h + i) * n_w + j] = __fadd_rn(acc, bias ? bias[k] : 0.0f);
+}
+
 // ------------------------------------------------------------------------------
 // fast 3x3 kernel
 // ------------------------------------------------------------------------------
@@ -467,6 +499,24 @@ int fscnn_sf_conv_exact(const float *x, int n, int c, int h, int w, const fscnn_
         x, c, h, w, reinterpret_cast<const int2 *>(nodes), seg_off, k, h_f, w_f, stride, pad, n_h,
         n_w, bias, relu, y);
     FSCNN_LAUNCH_CHECK("sf_exact_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_dense_conv_exact(const float *x, int n, int c, int h, int w, const float *wt, int k,
+                           int h_f, int w_f, int stride, int pad, const float *bias, float *y,
+                           void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
+    FSCNN_REQUIRE(h_f > 0 && w_f > 0 && stride > 0 && pad >= 0, "bad geometry");
+    FSCNN_REQUIRE(h_f <= h + 2 * pad && w_f <= w + 2 * pad, "filter exceeds padded input");
+    int n_h = (h + 2 * pad - h_f) / stride + 1;
+    int n_w = (w + 2 * pad - w_f) / stride + 1;
+    if (n == 0 || k == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && wt && y, "null buffer");
+    FSCNN_REQUIRE(k <= 65535 && n <= 65535, "k or n too large for the grid");
+    dim3 grid((unsigned)ceil_div((int64_t)n_h * n_w, 128), (unsigned)k, (unsigned)n);
+    dense_exact_kernel<<<grid, 128, 0, as_stream(stream)>>>(x, c, h, w, wt, k, h_f, w_f, stride, pad,
+                                                            n_h, n_w, bias, y);
+    FSCNN_LAUNCH_CHECK("dense_exact_kernel");
     return FSCNN_OK;
 }
 

@@ -63,11 +63,13 @@ class Encoded:
 
 
 def encode(src: torch.Tensor, batch: int, outer: int, mid: int, inner: int,
-           strides: tuple[int, int, int, int], slack: int = 0) -> Encoded:
+           strides: tuple[int, int, int, int], slack: int = 0, mask: torch.Tensor | None = None) -> Encoded:
     """Node-format encoding of ``batch`` arranged (outer, mid, inner) views of ``src``.
 
     strides = (s_b, s_o, s_m, s_i) in elements.  Restates sparsify_tensor3 /
     SparseTensor4.stack (sparse_core.py:273-353) on the device; see fscnn_encode_*.
+    With ``mask`` (uint8, same element offsets as ``src``) an entry is stored iff its
+    mask byte is set (fscnn_encode_masked_*), whatever its value.
     """
     dev = _dev()
     s_b, s_o, s_m, s_i = (int(v) for v in strides)
@@ -77,16 +79,23 @@ def encode(src: torch.Tensor, batch: int, outer: int, mid: int, inner: int,
     ws_bytes = int(_lib.load().fscnn_encode_workspace_bytes(n_seg))
     ws = torch.empty(ws_bytes // 8 + 1, dtype=torch.int64, device=dev)
     st = stream()
-    call("fscnn_encode_offsets", ptr(src), batch, outer, mid, inner, s_b, s_o, s_m, s_i,
-         ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
+    geo = (batch, outer, mid, inner, s_b, s_o, s_m, s_i)
+    if mask is None:
+        call("fscnn_encode_offsets", ptr(src), *geo, ptr(seg), ptr(total), ptr(ws), ws_bytes, st)
+    else:
+        call("fscnn_encode_masked_offsets", ptr(src), ptr(mask), *geo, ptr(seg), ptr(total), ptr(ws),
+             ws_bytes, st)
     n_nodes = int(total.item())  # the format's one forced sync: size the node buffer
     nodes = torch.empty((n_nodes + slack, 2), dtype=torch.int32, device=dev)
     if slack:
         nodes[n_nodes:].fill_(-1)
     mat = torch.empty(max(batch * outer, 1), dtype=torch.int64, device=dev)
     ten = torch.empty(max(batch, 1), dtype=torch.int64, device=dev)
-    call("fscnn_encode_nodes", ptr(src), batch, outer, mid, inner, s_b, s_o, s_m, s_i,
-         ptr(seg), ptr(nodes), ptr(mat), ptr(ten), st)
+    if mask is None:
+        call("fscnn_encode_nodes", ptr(src), *geo, ptr(seg), ptr(nodes), ptr(mat), ptr(ten), st)
+    else:
+        call("fscnn_encode_masked_nodes", ptr(src), ptr(mask), *geo, ptr(seg), ptr(nodes), ptr(mat),
+             ptr(ten), st)
     return Encoded(nodes, n_nodes, seg[:n_seg], mat[: batch * outer], ten[:batch])
 
 
@@ -101,37 +110,47 @@ ORDER_AXES = {
 }
 
 
-def encode_order(x: torch.Tensor, order: str, slack: int = 0) -> Encoded:
-    """Encode a [B, C, H, W]-indexed tensor (any strides) in the named axis order."""
-    assert x.dim() == 4
+def _order_geometry(shape, strides, order: str):
+    """(outer, mid, inner, s_b, s_o, s_m, s_i) of a [B, C, H, W]-indexed view in ``order``."""
     inner_ax, mid_ax, outer_ax = ORDER_AXES[order]
-    dims = x.shape[1:]
-    st = x.stride()
-    es = (st[1], st[2], st[3])  # element strides of c, h, w
-    return encode(x, x.shape[0], dims[outer_ax], dims[mid_ax], dims[inner_ax],
-                  (st[0], es[outer_ax], es[mid_ax], es[inner_ax]), slack)
+    dims = shape[1:]
+    es = (strides[1], strides[2], strides[3])  # element strides of c, h, w
+    return (int(dims[outer_ax]), int(dims[mid_ax]), int(dims[inner_ax]),
+            int(strides[0]), int(es[outer_ax]), int(es[mid_ax]), int(es[inner_ax]))
+
+
+def encode_order(x: torch.Tensor, order: str, slack: int = 0, mask: torch.Tensor | None = None) -> Encoded:
+    """Encode a [B, C, H, W]-indexed tensor (any strides) in the named axis order; with
+    ``mask`` (same strides) the stored set is the mask, not the nonzeros."""
+    assert x.dim() == 4
+    if mask is not None:
+        assert mask.stride() == x.stride() and mask.dtype == torch.uint8
+    o, m, i, s_b, s_o, s_m, s_i = _order_geometry(x.shape, x.stride(), order)
+    return encode(x, x.shape[0], o, m, i, (s_b, s_o, s_m, s_i), slack, mask)
 
 
 def decode(nodes: torch.Tensor, seg_off: torch.Tensor, batch: int, outer: int, mid: int,
-           inner: int, out: torch.Tensor, strides: tuple[int, int, int, int]) -> torch.Tensor:
-    """Write every element of the strided destination view from node format."""
+           inner: int, out: torch.Tensor, strides: tuple[int, int, int, int],
+           mask: torch.Tensor | None = None) -> torch.Tensor:
+    """Write every element of the strided destination view from node format (and, with
+    ``mask``, 1 where a node is stored / 0 elsewhere at the same element offsets)."""
     d_b, d_o, d_m, d_i = (int(v) for v in strides)
-    call("fscnn_decode", ptr(nodes), ptr(seg_off), batch, outer, mid, inner, ptr(out),
-         d_b, d_o, d_m, d_i, stream())
+    if mask is None:
+        call("fscnn_decode", ptr(nodes), ptr(seg_off), batch, outer, mid, inner, ptr(out),
+             d_b, d_o, d_m, d_i, stream())
+    else:
+        call("fscnn_decode_masked", ptr(nodes), ptr(seg_off), batch, outer, mid, inner, ptr(out),
+             ptr(mask), d_b, d_o, d_m, d_i, stream())
     return out
 
 
-def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None = None):
+def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None = None,
+                 mask: torch.Tensor | None = None):
     """Inverse of encode_order: returns a dense [B, C, H, W] tensor."""
-    b = dims_bchw[0]
-    dims = dims_bchw[1:]
     if out is None:
         out = torch.empty(tuple(dims_bchw), dtype=torch.float32, device=_dev())
-    inner_ax, mid_ax, outer_ax = ORDER_AXES[order]
-    st = out.stride()
-    es = (st[1], st[2], st[3])
-    return decode(nodes, seg_off, b, dims[outer_ax], dims[mid_ax], dims[inner_ax], out,
-                  (st[0], es[outer_ax], es[mid_ax], es[inner_ax]))
+    o, m, i, s_b, s_o, s_m, s_i = _order_geometry(out.shape, out.stride(), order)
+    return decode(nodes, seg_off, int(dims_bchw[0]), o, m, i, out, (s_b, s_o, s_m, s_i), mask)
 
 
 # -- sparse-filter conv ------------------------------------------------------------------
@@ -359,6 +378,75 @@ def relu(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty_like(x)
     call("fscnn_relu", ptr(x), x.numel(), ptr(out), stream())
+    return out
+
+
+ACT_RELU, ACT_LEAKY, ACT_RELU_NODES = 0, 1, 2
+
+
+def activation(x: torch.Tensor, kind: int, slope: float = 0.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """ACT_RELU: np.maximum(x, 0); ACT_LEAKY: np.where(x > 0, x, slope*x);
+    ACT_RELU_NODES: x > 0 ? x : 0 (the node-format keep rule, layers.py:488-489)."""
+    x = x.contiguous()
+    if out is None:
+        out = torch.empty_like(x)
+    call("fscnn_activation", ptr(x), x.numel(), int(kind), float(np.float32(slope)), ptr(out), stream())
+    return out
+
+
+def batchnorm(x: torch.Tensor, scale, shift, mean, var, eps: float, out=None) -> torch.Tensor:
+    """apply_batchnorm (layers.py:507-509) on NCHW, numpy float32 op order."""
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    dev = x.device
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+    sc, sh, mu, va = t(scale), t(shift), t(mean), t(var)
+    if out is None:
+        out = torch.empty_like(x)
+    call("fscnn_batchnorm", ptr(x), n, c, h, w, ptr(sc), ptr(sh), ptr(mu), ptr(va),
+         float(np.float32(eps)), ptr(out), stream())
+    return out
+
+
+def pad2d(x: torch.Tensor, p: int, out=None) -> torch.Tensor:
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    if out is None:
+        out = torch.empty((n, c, h + 2 * p, w + 2 * p), dtype=torch.float32, device=x.device)
+    call("fscnn_pad2d", ptr(x), n, c, h, w, int(p), ptr(out), stream())
+    return out
+
+
+def remap_segments(nodes: torch.Tensor, seg_off: torch.Tensor, n_nodes: int, seg_map: torch.Tensor):
+    """Segment gather (see fscnn_remap_segments_*): returns (nodes, n_nodes, seg_off)."""
+    dev = _dev()
+    n_old, n_new = int(seg_off.numel()), int(seg_map.numel())
+    new_off = torch.empty(max(n_new, 1), dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)
+    ws_bytes = int(_lib.load().fscnn_encode_workspace_bytes(n_new))
+    ws = torch.empty(ws_bytes // 8 + 1, dtype=torch.int64, device=dev)
+    m = seg_map.to(dev, torch.int64).contiguous()
+    call("fscnn_remap_segments_offsets", ptr(seg_off), n_old, n_nodes, ptr(m), n_new, ptr(new_off),
+         ptr(total), ptr(ws), ws_bytes, stream())
+    count = int(total.item())
+    out = torch.empty((max(count, 1), 2), dtype=torch.int32, device=dev)
+    call("fscnn_remap_segments_nodes", ptr(nodes), ptr(seg_off), n_old, n_nodes, ptr(m), n_new,
+         ptr(new_off), ptr(out), stream())
+    return out[:count], count, new_off[:n_new]
+
+
+def dense_conv_exact(x: torch.Tensor, wt: torch.Tensor, stride_: int, pad: int, bias: torch.Tensor | None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """Dense baseline conv, bit-exact with _dense_conv_kernel (kernels.py:169-192)."""
+    x, wt = x.contiguous(), wt.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    k, _, h_f, w_f = (int(v) for v in wt.shape)
+    n_h = (h + 2 * pad - h_f) // stride_ + 1
+    n_w = (w + 2 * pad - w_f) // stride_ + 1
+    if out is None:
+        out = torch.empty((n, k, n_h, n_w), dtype=torch.float32, device=x.device)
+    call("fscnn_dense_conv_exact", ptr(x), n, c, h, w, ptr(wt), k, h_f, w_f, stride_, pad, ptr(bias),
+         ptr(out), stream())
     return out
 
 

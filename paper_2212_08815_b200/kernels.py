@@ -1,9 +1,12 @@
-"""Convolution operators -- drop-in for sparse_infer.kernels (the hot-path subset).
+"""Convolution operators -- drop-in for sparse_infer.kernels.
 
-``conv_dense_input_sparse_filter[_counted]`` (kernels.py:264-305) and
-``conv_sparse_input_dense_filter`` (kernels.py:308-339) keep the reference's
+``conv_dense_input_sparse_filter[_counted]`` (kernels.py:264-305),
+``conv_sparse_input_dense_filter`` (kernels.py:308-339), ``dense_conv_reference``
+(:342-350), ``dot_dense_sparse`` (:352-358) and the node-format transposes
+``transpose_matrix`` / ``transpose_tensor3`` (:360-411) keep the reference's
 signatures, validation and error messages; the arithmetic runs on the GPU in the
-reference's accumulation order (bit-exact; see fscnn_sf_conv_exact / fscnn_si_conv).
+reference's accumulation order (bit-exact; see fscnn_sf_conv_exact / fscnn_si_conv /
+fscnn_dense_conv_exact), and the transposes move nodes without touching values.
 """
 
 from __future__ import annotations
@@ -19,6 +22,7 @@ from .sparse_core import (
     FormatError,
     SparseMatrix,
     SparseTensor3,
+    SparseVector,
 )
 
 
@@ -174,3 +178,70 @@ def conv_sparse_input_dense_filter(t_in: SparseTensor3, t_f: DenseTensor3, geom:
     enc = device.encode(y, 1, 1, geom.n_h, geom.n_w, (0, 0, geom.n_w, 1))
     return SparseMatrix(AxisOrder2.WH, geom.n_h, geom.n_w, device.nodes_to_numpy(enc.nodes, enc.n_nodes),
                         enc.seg_off.cpu().numpy())
+
+
+def dense_conv_reference(t_in: DenseTensor3, t_f: DenseTensor3, geom: ConvGeometry) -> np.ndarray:
+    """Dense cross-correlation with one filter (kernels.py:342-350): the GPU dense kernel
+    in _dense_conv_kernel's (kh, kw, c) order, bit-exact."""
+    _check_conv_args(t_in.dims, t_f.dims, geom)
+    from . import device
+
+    y = device.dense_conv_exact(dense_to_device(t_in), filters_to_device_kcrs([t_f]), geom.stride,
+                                geom.padding, None)
+    return y[0, 0].cpu().numpy()
+
+
+def dot_dense_sparse(d: np.ndarray, s: SparseVector) -> float:
+    """Inner product of a dense fiber with a sparse vector in node order (kernels.py:352-358):
+    the reference-order sparse-filter kernel on a 1x1 "image" of len(d) channels."""
+    d = np.ascontiguousarray(d, dtype=np.float32)
+    s.validate()
+    if s.length > len(d):
+        raise FormatError(f"sparse length {s.length} exceeds dense length {len(d)}")
+    torch = _torch()
+    from . import device
+
+    x = torch.from_numpy(d).cuda().view(1, len(d), 1, 1)
+    nodes = device.nodes_from_numpy(s.nodes)
+    seg = torch.zeros(1, dtype=torch.int64, device="cuda")
+    return float(device.sf_conv_exact(x, nodes, seg, 1, 1, 1, 1, 0, None)[0, 0, 0, 0].item())
+
+
+def transpose_matrix(m: SparseMatrix) -> SparseMatrix:
+    """WH <-> HW storage switch (kernels.py:360-380) on the GPU: decode with a presence
+    mask, masked re-encode in the other order -- every stored node (explicit zeros
+    too) moves with its value untouched."""
+    torch = _torch()
+    from . import device
+
+    dense = torch.zeros((m.n_rows, m.n_cols), dtype=torch.float32, device="cuda")
+    mask = torch.zeros((m.n_rows, m.n_cols), dtype=torch.uint8, device="cuda")
+    row_major = (0, 0, m.n_cols, 1)   # WH: segment = row, index = column
+    col_major = (0, 0, 1, m.n_cols)   # HW: segment = column, index = row
+    src, dst = (row_major, col_major) if m.order is AxisOrder2.WH else (col_major, row_major)
+    if m.n_segments and m.segment_length:
+        device.decode(device.nodes_from_numpy(m.nodes), torch.from_numpy(np.asarray(m.segment_offsets, np.int64)).cuda(),
+                      1, 1, m.n_segments, m.segment_length, dense, src, mask)
+    flipped = AxisOrder2.HW if m.order is AxisOrder2.WH else AxisOrder2.WH
+    n_seg, seg_len = (m.n_cols, m.n_rows) if flipped is AxisOrder2.HW else (m.n_rows, m.n_cols)
+    enc = device.encode(dense, 1, 1, n_seg, seg_len, dst, mask=mask)
+    return SparseMatrix(flipped, m.n_rows, m.n_cols, device.nodes_to_numpy(enc.nodes, enc.n_nodes),
+                        enc.seg_off.cpu().numpy())
+
+
+def transpose_tensor3(t: SparseTensor3) -> SparseTensor3:
+    """WHC -> CHW without touching any value (kernels.py:383-411), on the GPU: masked
+    decode from WHC, masked encode in CHW."""
+    _require_order3(t, AxisOrder3.WHC, "tensor")
+    torch = _torch()
+    from . import device
+
+    c, h, w = t.dims
+    dense = torch.zeros((1, c, h, w), dtype=torch.float32, device="cuda")
+    mask = torch.zeros((1, c, h, w), dtype=torch.uint8, device="cuda")
+    if t.n_segments:
+        device.decode_order(device.nodes_from_numpy(t.nodes), torch.from_numpy(np.asarray(t.segment_offsets, np.int64)).cuda(),
+                            (1, c, h, w), "WHC", out=dense, mask=mask)
+    enc = device.encode_order(dense, "CHW", mask=mask)
+    return SparseTensor3(AxisOrder3.CHW, tuple(t.dims), device.nodes_to_numpy(enc.nodes, enc.n_nodes),
+                         enc.matrix_off.cpu().numpy(), enc.seg_off.cpu().numpy())

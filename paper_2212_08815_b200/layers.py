@@ -248,23 +248,133 @@ def pool_standalone(t: DenseTensor3, pool, mode: str) -> DenseTensor3:
     return kernels.dense_from_device(y)
 
 
-def apply_activation(t, kind: str, slope: float = 0.0):
-    """ReLU on dense tensors (layers.py:469-484) on the GPU.
+def pool_sparse(t: SparseTensor3, pool, mode: str) -> SparseTensor3:
+    """Node-format pooling (layers.py:464-466): decode, pool, re-encode in t.order -- all
+    on the GPU, no host round trip in between."""
+    from . import device
+    from .sparse_core import from_device_dense, to_device_dense
 
-    LeakyReLU and node-format activations belong to the sparse-input pipeline
-    (not built yet) and raise NotImplementedError.
+    c, h, w = t.dims
+    h_p, w_p = pool
+    if h_p <= 0 or w_p <= 0:
+        raise ValueError(f"pool window must be positive, got {pool}")
+    if h % h_p or w % w_p:
+        raise ValueError(f"input {h}x{w} not divisible by pool window {h_p}x{w_p}")
+    if mode not in (POOL_MAX, POOL_AVG):
+        raise ValueError(f"unknown pool mode {mode!r}")
+    y = device.pool2d(to_device_dense(t), h_p, w_p, mode == POOL_MAX)
+    return from_device_dense(y, t.order)
+
+
+def apply_activation(t, kind: str, slope: float = 0.0):
+    """ReLU / LeakyReLU keeping the representation (layers.py:469-492), on the GPU.
+
+    Dense: np.maximum(x, 0) / np.where(x > 0, x, s*x).  Node format: the reference's
+    rebuild_tensor3 (sparse_core.py:460-473) -- ReLU keeps nodes with value > 0 (NaN and
+    -0.0 dropped), LeakyReLU rescales negative nodes and keeps the nonzero results --
+    done as decode -> elementwise -> re-encode, which yields the same nodes and offsets
+    because a valid segment's indices ascend.
     """
     if kind not in ("relu", "leaky_relu"):
         raise ValueError(f"unknown activation {kind!r}")
     if slope < 0:
         raise ValueError("leaky slope must be non-negative")
-    if isinstance(t, DenseTensor3) and kind == "relu":
-        import torch
+    from . import device
 
-        from . import device
+    if isinstance(t, DenseTensor3):
+        flat = kernels._torch().from_numpy(np.ascontiguousarray(t.data)).cuda()
+        y = device.activation(flat, device.ACT_RELU if kind == "relu" else device.ACT_LEAKY, slope)
+        return DenseTensor3(tuple(t.dims), y.cpu().numpy())
+    if isinstance(t, SparseTensor3):
+        from .sparse_core import from_device_dense, to_device_dense
 
-        flat = torch.from_numpy(np.ascontiguousarray(t.data)).cuda()
-        return DenseTensor3(tuple(t.dims), device.relu(flat).cpu().numpy())
-    if isinstance(t, (DenseTensor3, SparseTensor3)):
-        raise NotImplementedError(f"{kind} on {type(t).__name__} is outside the built hot path (SURVEY.md §8f-1)")
+        act = device.ACT_RELU_NODES if kind == "relu" else device.ACT_LEAKY
+        return from_device_dense(device.activation(to_device_dense(t), act, slope), t.order)
     raise TypeError(f"apply_activation does not support {type(t).__name__}")
+
+
+@dataclass(frozen=True)
+class BatchNormParams:
+    """Per-channel inference statistics, all float32 incl. epsilon (layers.py:108-133)."""
+
+    scale: np.ndarray
+    shift: np.ndarray
+    mean: np.ndarray
+    var: np.ndarray
+    epsilon: float = 1e-5
+
+    def __post_init__(self):
+        for name in ("scale", "shift", "mean", "var"):
+            object.__setattr__(self, name, np.asarray(getattr(self, name), dtype=np.float32))
+        object.__setattr__(self, "epsilon", float(np.float32(self.epsilon)))
+
+    def validate(self, channels: int) -> None:
+        for name in ("scale", "shift", "mean", "var"):
+            if getattr(self, name).shape != (channels,):
+                raise ValueError(f"batchnorm {name} must have shape ({channels},)")
+        if np.any(self.var + np.float32(self.epsilon) <= 0):
+            raise ValueError("batchnorm requires var + epsilon > 0 per channel")
+
+
+def apply_batchnorm(t, params: BatchNormParams):
+    """Inference batch norm (layers.py:495-510) on the GPU; node-format input is decoded,
+    normalised and re-encoded in its order (the result is dense in general)."""
+    from . import device
+
+    params.validate(t.dims[0])
+    if isinstance(t, SparseTensor3):
+        from .sparse_core import from_device_dense, to_device_dense
+
+        y = device.batchnorm(to_device_dense(t), params.scale, params.shift, params.mean, params.var,
+                             params.epsilon)
+        return from_device_dense(y, t.order)
+    if not isinstance(t, DenseTensor3):
+        raise TypeError(f"apply_batchnorm does not support {type(t).__name__}")
+    y = device.batchnorm(kernels.dense_to_device(t), params.scale, params.shift, params.mean, params.var,
+                         params.epsilon)
+    return kernels.dense_from_device(y)
+
+
+def pad_tensor(t, p: int):
+    """Zero-pad the spatial extents by p (layers.py:513-540).  CHW node tensors keep every
+    node (explicit zeros too): only segment placement changes, a device segment gather."""
+    if p < 0:
+        raise ValueError("pad width must be non-negative")
+    if p == 0:
+        return t
+    from . import device
+
+    if isinstance(t, DenseTensor3):
+        return kernels.dense_from_device(device.pad2d(kernels.dense_to_device(t), p))
+    if isinstance(t, SparseTensor3):
+        from .sparse_core import from_device_dense, to_device_dense
+
+        if t.order is not AxisOrder3.CHW:
+            return from_device_dense(device.pad2d(to_device_dense(t), p), t.order)
+        torch = kernels._torch()
+        c, h, w = t.dims
+        nh, nw = h + 2 * p, w + 2 * p
+        # new segment w'*nh + h' <- old (w'-p)*h + (h'-p) inside, else empty
+        wi = torch.arange(nw, device="cuda").view(nw, 1) - p
+        hi = torch.arange(nh, device="cuda").view(1, nh) - p
+        inside = (wi >= 0) & (wi < w) & (hi >= 0) & (hi < h)
+        seg_map = torch.where(inside, wi * h + hi, torch.full_like(wi * hi, -1)).view(-1)
+        nodes, n_nodes = device.nodes_from_numpy(t.nodes), len(t.nodes)
+        seg = torch.from_numpy(np.asarray(t.segment_offsets, np.int64)).cuda()
+        out, count, off = device.remap_segments(nodes, seg, n_nodes, seg_map)
+        off_h = off.cpu().numpy()
+        return SparseTensor3(t.order, (c, nh, nw), device.nodes_to_numpy(out, count), off_h[::nh].copy(), off_h)
+    raise TypeError(f"pad_tensor does not support {type(t).__name__}")
+
+
+def conv_forward_dense(t_in: DenseTensor3, filters: list[DenseTensor3], stride: int, padding: int,
+                       bias: np.ndarray, workers: int = 1) -> DenseTensor3:
+    """The 100%-density baseline layer (layers.py:326-342): every weight multiplied, in
+    _dense_conv_kernel's order, + bias -- one bit-exact GPU launch for all filters."""
+    from . import device
+
+    geom = ConvGeometry(tuple(t_in.dims), tuple(filters[0].dims), stride, padding)
+    kcrs = kernels.filters_to_device_kcrs(filters)
+    b = kernels._torch().from_numpy(np.ascontiguousarray(bias, dtype=np.float32)).cuda()
+    y = device.dense_conv_exact(kernels.dense_to_device(t_in), kcrs, geom.stride, geom.padding, b)
+    return kernels.dense_from_device(y)

@@ -1,15 +1,20 @@
-"""Network orchestration -- drop-in for the sparse-filter VGG path of sparse_infer.network.
+"""Network orchestration -- drop-in for sparse_infer.network.
 
-``build_benchmark_net``, ``prepare`` and ``forward`` keep the reference's names,
-signatures, validation messages and report fields (network.py:297-602).  ``prepare``
-encodes every conv bank on the GPU (bit-exact SparseTensor4, as network.py:371-377)
-and, for the conv3x3 -> relu [-> maxpool 2x2] stacks of ``vgg16_desk``, binds a
-device-resident VGGEngine: ``forward`` then stages the whole batch (pinned H2D, GPU
-layout conversion), runs one fused kernel per conv, and copies the outputs back.
-Other stacks built from conv / relu / maxpool / avgpool run layer by layer through
-the GPU operators in layers.py.  Batch norm, leaky ReLU, pad and the sparse-input
-variant's node-format pipeline are outside the built hot path and
-raise NotImplementedError.
+``build_benchmark_net``, ``prepare``, ``forward``, ``random_weights``,
+``prune_weights`` and ``density_evolution`` keep the reference's names, signatures,
+validation messages and report fields (network.py:170-643).  All three variants run
+on the GPU:
+
+* sparse_filter: ``prepare`` encodes every conv bank on the GPU (bit-exact
+  SparseTensor4, network.py:371-377); for conv3x3 -> relu [-> maxpool 2x2] stacks
+  (``vgg16_desk``) it binds a device-resident VGGEngine, so ``forward`` stages the
+  whole batch (pinned H2D, GPU layout conversion), runs one fused kernel per conv and
+  copies the outputs back;
+* sparse_input: node-format activations through the sparse-input conv, node-format
+  ReLU / LeakyReLU / pooling, and the conv + pool fusion rule of network.py:380-389;
+* dense_baseline: the dense conv in the reference's order.
+Other stacks (and density recording) run layer by layer through the GPU operators in
+layers.py, exactly following the reference's step logic (network.py:410-461).
 """
 
 from __future__ import annotations
@@ -120,6 +125,8 @@ def build_benchmark_net(kind: str, scale: float, input_hw: int = 32, variant: st
 
 @dataclass
 class _Step:
+    """One runnable step; a fused conv + pool step consumes two layer indices."""
+
     layer_index: int
     kind: str
     params: object = None
@@ -127,6 +134,10 @@ class _Step:
     stride: int = 1
     padding: int = 0
     kernel: tuple[int, int] = (0, 0)
+    slope: float = 0.0
+    fused_pool: tuple[int, int] | None = None
+    fused_pool_mode: str = ly.POOL_MAX
+    fused_layer_index: int = -1
 
 
 @dataclass
@@ -178,38 +189,58 @@ def _vgg_plan(net: NetworkSpec):
 
 
 def prepare(net: NetworkSpec, weights: NetworkWeights) -> PreparedNet:
-    """Bind weights: GPU-encode every conv bank (network.py:345-407)."""
-    from .sparse_core import sparsify_tensor3  # noqa: F401  (GPU encoder)
+    """Bind weights in the representation the variant needs (network.py:345-407).
 
-    if net.variant != VARIANT_SPARSE_FILTER:
-        raise NotImplementedError(f"variant {net.variant!r} is outside the built hot path (SURVEY.md §8f-1)")
+    sparse_filter: GPU-encoded CHW SparseTensor4 banks; other variants: dense filter
+    lists.  On sparse_input a bias-free conv directly followed by a pool whose window
+    divides the conv output fuses into one step that consumes the pool layer.
+    """
     params = dict(zip((li for li, _ in parameterized_layers(net)), weights.entries))
+    chain = [net.input_dims] + net.shape_chain()
     steps = []
-    convs = []
+    skip = -1
     for li, layer in enumerate(net.layers):
+        if li == skip:
+            continue
         if layer.kind == "conv":
             entry = params[li]
             if not isinstance(entry, ConvParams):
                 raise ValueError(f"layer {li} expects conv parameters")
-            bank = _encode_bank(np.asarray(entry.filters, np.float32))
-            steps.append(_Step(li, "conv", bank, np.asarray(entry.bias, np.float32), layer.stride, layer.padding,
-                               tuple(layer.kernel)))
-            convs.append((np.asarray(entry.filters, np.float32), np.asarray(entry.bias, np.float32)))
-        elif layer.kind in ("relu", "maxpool", "avgpool"):
-            steps.append(_Step(li, layer.kind, kernel=tuple(layer.kernel)))
+            filters = np.asarray(entry.filters, np.float32)
+            step = _Step(li, "conv", bias=np.asarray(entry.bias, np.float32), stride=layer.stride,
+                         padding=layer.padding, kernel=tuple(layer.kernel))
+            if net.variant == VARIANT_SPARSE_FILTER:
+                step.params = _encode_bank(filters)
+            else:
+                step.params = [DenseTensor3.from_array(f) for f in filters]
+            if net.variant == VARIANT_SPARSE_INPUT and li + 1 < len(net.layers):
+                nxt = net.layers[li + 1]
+                if nxt.kind in ("maxpool", "avgpool") and not np.any(step.bias != 0):
+                    _, h, w = chain[li + 1]
+                    h_p, w_p = nxt.kernel
+                    if h % h_p == 0 and w % w_p == 0:
+                        step.fused_pool = tuple(nxt.kernel)
+                        step.fused_pool_mode = ly.POOL_MAX if nxt.kind == "maxpool" else ly.POOL_AVG
+                        step.fused_layer_index = li + 1
+                        skip = li + 1
+            steps.append(step)
+        elif layer.kind == "batchnorm":
+            entry = params[li]
+            if not isinstance(entry, ly.BatchNormParams):
+                raise ValueError(f"layer {li} expects batchnorm parameters")
+            entry.validate(chain[li][0])
+            steps.append(_Step(li, "batchnorm", params=entry))
         else:
-            raise NotImplementedError(f"layer kind {layer.kind!r} is outside the built hot path (SURVEY.md §8f)")
+            steps.append(_Step(li, layer.kind, kernel=tuple(layer.kernel), padding=layer.padding,
+                               slope=layer.slope))
     engine = None
-    plan = _vgg_plan(net)
+    plan = _vgg_plan(net) if net.variant == VARIANT_SPARSE_FILTER else None
     if plan is not None:
         from .engine import VGGEngine
 
-        encoded = []
-        for st in steps:
-            if st.kind == "conv":
-                encoded.append(st.params)
+        convs = [st for st in steps if st.kind == "conv"]
         engine = VGGEngine(None, batch=1, hw=net.input_dims[1], plan=plan, in_c=net.input_dims[0],
-                           encoded=[_device_encoded(b, s.bias) for b, s in zip(encoded, [s for s in steps if s.kind == "conv"])])
+                           encoded=[_device_encoded(st.params, st.bias) for st in convs])
     return PreparedNet(net=net, steps=steps, n_layers=len(net.layers), engine=engine)
 
 
@@ -307,14 +338,33 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
     return [DenseTensor3((oc, ohw, ohw), out[i].copy()) for i in range(n)]
 
 
-def _run_step(step: _Step, x):
+def _run_step(step: _Step, x, variant: str, strat):
+    """One step (network.py:410-448), every branch a GPU operator."""
     if step.kind == "conv":
-        return ly.conv_forward_strategy_II(x, step.params, step.stride, step.padding, step.bias)
+        if isinstance(x, SparseTensor3):
+            return ly.conv_forward_sparse_input(x, step.params, step.stride, step.padding, step.bias,
+                                                fused_pool=step.fused_pool, pool_mode=step.fused_pool_mode)
+        if variant == VARIANT_SPARSE_FILTER:
+            if strat is ly.StrategyKind.STRATEGY_I:
+                return ly.conv_forward_strategy_I(x, step.params, step.stride, step.padding, step.bias)
+            return ly.conv_forward_strategy_II(x, step.params, step.stride, step.padding, step.bias)
+        out = ly.conv_forward_dense(x, step.params, step.stride, step.padding, step.bias)
+        if step.fused_pool is not None:
+            # an upstream biased conv turned the pipeline dense; the consumed pool still runs
+            out = ly.pool_standalone(out, step.fused_pool, step.fused_pool_mode)
+        return out
     if step.kind in ("maxpool", "avgpool"):
-        return ly.pool_standalone(x, step.kernel, ly.POOL_MAX if step.kind == "maxpool" else ly.POOL_AVG)
-    if step.kind == "relu":
-        return ly.apply_activation(x, "relu")
-    raise NotImplementedError(f"step kind {step.kind!r}")
+        mode = ly.POOL_MAX if step.kind == "maxpool" else ly.POOL_AVG
+        if isinstance(x, SparseTensor3):
+            return ly.pool_sparse(x, step.kernel, mode)
+        return ly.pool_standalone(x, step.kernel, mode)
+    if step.kind in ("relu", "leaky_relu"):
+        return ly.apply_activation(x, step.kind, step.slope)
+    if step.kind == "batchnorm":
+        return ly.apply_batchnorm(x, step.params)
+    if step.kind == "pad":
+        return ly.pad_tensor(x, step.padding)
+    raise ValueError(f"unknown step kind {step.kind!r}")
 
 
 def forward(prepared: PreparedNet, batch: list, workers: int = 1,
@@ -335,9 +385,12 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
         for t in batch:
             x = t
             for step in prepared.steps:
-                x = _run_step(step, x)
+                x = _run_step(step, x, variant, strat)
                 if densities is not None:
                     densities[step.layer_index].append(density(x))
+                    if step.fused_layer_index >= 0:
+                        # the conv intermediate never materialises: both layers see the pool
+                        densities[step.fused_layer_index].append(density(x))
             outputs.append(x)
     seconds = time.perf_counter() - t0
     layer_densities = None
@@ -347,3 +400,72 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
                        strategy=strat.name.lower() if variant == VARIANT_SPARSE_FILTER else "-",
                        seconds=seconds, layer_densities=layer_densities)
     return ForwardResult(outputs=outputs, report=report)
+
+
+# -- weights and the density-evolution study (network.py:170-207, :605-643) ----------
+
+
+def random_weights(net: NetworkSpec, seed: int) -> NetworkWeights:
+    """Filters uniform on [-0.5, 0.5], zero biases, batch-norm statistics uniform with
+    var in [0.5, 1.5]; one numpy generator per layer seeded [seed, layer] (host-side
+    workload generation, draw order as network.py:173-195)."""
+    chain = [net.input_dims] + net.shape_chain()
+    entries = []
+    for li, layer in parameterized_layers(net):
+        rng = np.random.default_rng([seed, li])
+        c_in = chain[li][0]
+        if layer.kind == "conv":
+            shape = (layer.out_channels, c_in) + tuple(layer.kernel)
+            entries.append(ConvParams(filters=rng.uniform(-0.5, 0.5, shape).astype(np.float32),
+                                      bias=np.zeros(layer.out_channels, np.float32)))
+        else:
+            draws = [rng.uniform(lo, hi, c_in).astype(np.float32)
+                     for lo, hi in ((0.5, 1.5), (-0.5, 0.5), (-0.5, 0.5), (0.5, 1.5))]
+            entries.append(ly.BatchNormParams(scale=draws[0], shift=draws[1], mean=draws[2], var=draws[3],
+                                              epsilon=1e-5))
+    return NetworkWeights(entries=entries)
+
+
+def prune_weights(weights: NetworkWeights, target_density: float, seed: int) -> NetworkWeights:
+    """Prune every conv bank jointly to the target density, generator [seed, entry]."""
+    from .sparse_core import prune_array
+
+    out = []
+    for i, entry in enumerate(weights.entries):
+        if isinstance(entry, ConvParams):
+            out.append(ConvParams(filters=prune_array(entry.filters, target_density, [seed, i]), bias=entry.bias))
+        else:
+            out.append(entry)
+    return NetworkWeights(entries=out)
+
+
+@dataclass
+class DensityRecord:
+    input_density: float
+    layer_index: int
+    layer_kind: str
+    output_density: float
+
+
+def random_input(dims, seed: int) -> DenseTensor3:
+    rng = np.random.default_rng([seed, 0xBA7C4])
+    return DenseTensor3.from_array(rng.uniform(-0.5, 0.5, dims).astype(np.float32))
+
+
+def density_evolution(net: NetworkSpec, input_density_sweep: list, seed: int) -> list:
+    """Per-layer output densities for each input density (network.py:621-643): record 0
+    is the pruned input, record i+1 the output of layer i -- every layer on the GPU."""
+    from .sparse_core import prune_random, sparsify_tensor3
+
+    if net.variant != VARIANT_SPARSE_INPUT:
+        raise ValueError("density evolution requires the sparse_input variant")
+    prepared = prepare(net, random_weights(net, seed))
+    base = random_input(net.input_dims, seed)
+    records = []
+    for d in input_density_sweep:
+        sp = sparsify_tensor3(prune_random(base, d, seed), AxisOrder3.CHW)
+        records.append(DensityRecord(d, 0, "input", density(sp)))
+        result = forward(prepared, [sp], record_density=True)
+        for li, layer in enumerate(net.layers):
+            records.append(DensityRecord(d, li + 1, layer.kind, result.report.layer_densities[li]))
+    return records

@@ -30,6 +30,18 @@ def nodes_from_i64(words):
     return np.ascontiguousarray(words, dtype=np.int64).view(NODE_DTYPE)
 
 
+def weights_sha(weights) -> str:
+    """sha256 over every entry's arrays, as tests/golden/make_golden.py::gen_pipeline."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for e in weights.entries:
+        names = ("filters", "bias") if hasattr(e, "filters") else ("scale", "shift", "mean", "var")
+        for a in names:
+            h.update(np.ascontiguousarray(np.asarray(getattr(e, a))).tobytes())
+    return h.hexdigest()
+
+
 def normwise_err(a, ref):
     """max|a - ref| / max|ref| (BASELINE.json north_star tolerance form)."""
     a = np.asarray(a, np.float64)

@@ -251,7 +251,150 @@ def gen_pool_relu(out):
     np.savez_compressed(os.path.join(out, "pool_relu.npz"), **payload)
 
 
+def _put_sparse(payload, key, t):
+    payload[f"{key}__order"] = np.array(t.order.name)
+    payload[f"{key}__dims"] = np.array(t.dims, np.int64)
+    payload[f"{key}__nodes"] = _nodes_i64(t.nodes)
+    payload[f"{key}__matrix_offsets"] = np.asarray(t.matrix_offsets, np.int64)
+    payload[f"{key}__segment_offsets"] = np.asarray(t.segment_offsets, np.int64)
+
+
+def _with_special_nodes(t, rng):
+    """Copy of t with some stored values replaced by +0.0, -0.0, NaN and negatives --
+    explicit nodes the reference's own encoder never emits, but valid containers."""
+    nodes = t.nodes.copy()
+    data = np.nonzero(nodes["index"] != -1)[0]
+    if data.size >= 4:
+        pick = rng.choice(data, size=4, replace=False)
+        nodes["value"][pick] = np.array([0.0, -0.0, np.nan, -1.5], np.float32)
+    return si.SparseTensor3(order=t.order, dims=t.dims, nodes=nodes, matrix_offsets=t.matrix_offsets,
+                            segment_offsets=t.segment_offsets)
+
+
+def gen_pipeline(out):
+    """The sparse-input pipeline and the remaining layer operators:
+    node-format ReLU / LeakyReLU, pool_sparse, batch norm, pad, the dense baseline conv,
+    dot_dense_sparse, the node-format transposes, the three network variants on the
+    desk-scale VGG16 / YOLO stacks, and the density-evolution study."""
+    rng = np.random.default_rng(2007)
+    payload = {}
+    orders = [o for o in si.AxisOrder3]
+    # node-format activations, pooling, batch norm, pad
+    for i in range(8):
+        dims = (int(rng.integers(1, 6)), 2 * int(rng.integers(1, 5)), 2 * int(rng.integers(1, 5)))
+        x = rand_input(rng, dims, 0.5)
+        t = si.sparsify_tensor3(si.DenseTensor3.from_array(x), orders[i % 6])
+        if i % 2:
+            t = _with_special_nodes(t, rng)
+        t.validate()
+        key = f"n{i}"
+        _put_sparse(payload, f"{key}_in", t)
+        _put_sparse(payload, f"{key}_relu", si.apply_activation(t, "relu"))
+        _put_sparse(payload, f"{key}_leaky", si.apply_activation(t, "leaky_relu", 0.1))
+        _put_sparse(payload, f"{key}_pool", si.pool_sparse(t, (2, 2), "max" if i % 3 else "avg"))
+        payload[f"{key}_pool__mode"] = np.array("max" if i % 3 else "avg")
+        _put_sparse(payload, f"{key}_pad", si.pad_tensor(t, 1 + i % 2))
+        payload[f"{key}_pad__p"] = np.array(1 + i % 2)
+        bn = si.BatchNormParams(scale=rng.uniform(0.5, 1.5, dims[0]).astype(np.float32),
+                                shift=rng.uniform(-0.5, 0.5, dims[0]).astype(np.float32),
+                                mean=rng.uniform(-0.5, 0.5, dims[0]).astype(np.float32),
+                                var=rng.uniform(0.5, 1.5, dims[0]).astype(np.float32), epsilon=1e-5)
+        for f in ("scale", "shift", "mean", "var"):
+            payload[f"{key}_bn__{f}"] = getattr(bn, f)
+        _put_sparse(payload, f"{key}_bn", si.apply_batchnorm(t, bn))
+        d = si.DenseTensor3.from_array(x)
+        payload[f"{key}_dense__x"] = x
+        payload[f"{key}_dense_bn__y"] = si.apply_batchnorm(d, bn).to_array()
+        payload[f"{key}_dense_leaky__y"] = si.apply_activation(d, "leaky_relu", 0.1).to_array()
+        payload[f"{key}_dense_pad__y"] = si.pad_tensor(d, 1 + i % 2).to_array()
+    payload["n_node_cases"] = np.array(8)
+    # dense baseline conv (layer + single filter) and the dot product
+    for i in range(10):
+        c, h_i, w_i, k, s, p, _ = rand_conv_case(rng, max_c=10, max_hw=16)
+        n_f = int(rng.integers(1, 5))
+        x = rand_input(rng, (c, h_i, w_i), 0.7)
+        bank = np.stack([rand_filter(rng, (c, k, k), 0.6) for _ in range(n_f)])
+        bias = rng.uniform(-0.2, 0.2, n_f).astype(np.float32)
+        t_in = si.DenseTensor3.from_array(x)
+        y = si.conv_forward_dense(t_in, [si.DenseTensor3.from_array(f) for f in bank], s, p, bias)
+        geom = si.ConvGeometry((c, h_i, w_i), (c, k, k), s, p)
+        payload[f"d{i}__x"], payload[f"d{i}__w"], payload[f"d{i}__bias"] = x, bank, bias
+        payload[f"d{i}__geom"] = np.array([s, p], np.int64)
+        payload[f"d{i}__y"] = y.to_array()
+        payload[f"d{i}__y0"] = si.dense_conv_reference(t_in, si.DenseTensor3.from_array(bank[0]), geom)
+    payload["n_dense_cases"] = np.array(10)
+    for i in range(6):
+        n = int(rng.integers(1, 40))
+        dv = rand_input(rng, (n,))
+        sv = si.SparseVector.from_dense(rand_input(rng, (int(rng.integers(1, n + 1)),), 0.4))
+        payload[f"dot{i}__d"] = dv
+        payload[f"dot{i}__length"] = np.array(sv.length)
+        payload[f"dot{i}__nodes"] = _nodes_i64(sv.nodes)
+        payload[f"dot{i}__y"] = np.array(si.dot_dense_sparse(dv, sv), np.float64)
+    # transposes (explicit zero-valued nodes must move untouched)
+    for i in range(6):
+        r, c = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        a = rand_input(rng, (r, c), 0.5)
+        order = si.AxisOrder2.WH if i % 2 == 0 else si.AxisOrder2.HW
+        m = si.sparsify_matrix(a, order)
+        if m.nnz >= 1:
+            nodes = m.nodes.copy()
+            nodes["value"][np.nonzero(nodes["index"] != -1)[0][0]] = 0.0
+            m = si.SparseMatrix(order=m.order, n_rows=m.n_rows, n_cols=m.n_cols, nodes=nodes,
+                                segment_offsets=m.segment_offsets)
+        mt = si.transpose_matrix(m)
+        for tag, mm in (("in", m), ("out", mt)):
+            payload[f"tm{i}_{tag}__order"] = np.array(mm.order.name)
+            payload[f"tm{i}_{tag}__shape"] = np.array([mm.n_rows, mm.n_cols], np.int64)
+            payload[f"tm{i}_{tag}__nodes"] = _nodes_i64(mm.nodes)
+            payload[f"tm{i}_{tag}__segment_offsets"] = np.asarray(mm.segment_offsets, np.int64)
+    for i in range(4):
+        dims = (int(rng.integers(1, 7)), int(rng.integers(1, 7)), int(rng.integers(1, 7)))
+        t = si.sparsify_tensor3(si.DenseTensor3.from_array(rand_input(rng, dims, 0.5)), si.AxisOrder3.WHC)
+        if i % 2:
+            t = _with_special_nodes(t, rng)
+        _put_sparse(payload, f"tt{i}_in", t)
+        _put_sparse(payload, f"tt{i}_out", si.transpose_tensor3(t))
+    # the three network variants (desk scale) with density recording
+    cases = [("vgg16_desk", "sparse_input"), ("vgg16_desk_noact", "sparse_input"),
+             ("vgg16_desk", "dense_baseline"), ("yolo_desk", "sparse_input"),
+             ("yolo_desk", "dense_baseline"), ("yolo_desk", "sparse_filter"),
+             ("yolo_desk_nobn", "sparse_input")]
+    for i, (kind, variant) in enumerate(cases):
+        net = nw.build_benchmark_net(kind, 0.125, input_hw=32, variant=variant)
+        weights = nw.random_weights(net, 2008 + i)
+        if variant == "sparse_filter":
+            weights = nw.prune_weights(weights, 0.3, 2008 + i)
+        prepared = nw.prepare(net, weights)
+        base = nw.random_input(net.input_dims, 2008 + i)
+        x = si.prune_random(base, 0.4, 2008 + i)
+        inp = si.sparsify_tensor3(x, si.AxisOrder3.CHW) if variant == "sparse_input" else x
+        res = nw.forward(prepared, [inp], record_density=True)
+        o = res.outputs[0]
+        key = f"net{i}"
+        payload[f"{key}__kind"], payload[f"{key}__variant"] = np.array(kind), np.array(variant)
+        payload[f"{key}__seed"] = np.array(2008 + i)
+        payload[f"{key}__x"] = x.to_array()
+        payload[f"{key}__densities"] = np.array(res.report.layer_densities, np.float64)
+        if isinstance(o, si.SparseTensor3):
+            _put_sparse(payload, f"{key}_out", o)
+        else:
+            payload[f"{key}_out__y"] = o.to_array()
+        payload[f"{key}__weights_sha"] = np.array(sha(*[np.asarray(getattr(e, a)) for e in weights.entries
+                                                         for a in (("filters", "bias") if hasattr(e, "filters")
+                                                                   else ("scale", "shift", "mean", "var"))]))
+    payload["n_net_cases"] = np.array(len(cases))
+    net = nw.build_benchmark_net("vgg16_desk", 0.125, input_hw=32, variant="sparse_input")
+    recs = nw.density_evolution(net, [0.1, 0.5, 1.0], 2020)
+    payload["evo__input"] = np.array([r.input_density for r in recs], np.float64)
+    payload["evo__layer"] = np.array([r.layer_index for r in recs], np.int64)
+    payload["evo__kind"] = np.array([r.layer_kind for r in recs])
+    payload["evo__density"] = np.array([r.output_density for r in recs], np.float64)
+    np.savez_compressed(os.path.join(out, "pipeline.npz"), **payload)
+
+
 def main():
+    gen_pipeline(HERE)
     gen_encoder(HERE)
     gen_sf(HERE)
     gen_si(HERE)

@@ -214,3 +214,25 @@ def test_shard_range_covers_batch():
 def test_node_dtype_is_reference_layout():
     assert NODE_DTYPE.itemsize == 8 and NODE_DTYPE.names == ("index", "value")
     assert fs.AxisOrder3.CHW.axes == (0, 1, 2) and fs.AxisOrder3.WHC.axes == (2, 1, 0)
+
+
+def test_weight_and_input_generators_match_reference():
+    """random_weights / prune_weights / random_input / prune_random are host-side
+    workload generators; they must reproduce the reference's draws exactly
+    (tests/golden/pipeline.npz, made by the reference)."""
+    from conftest import load_golden, weights_sha
+
+    from paper_2212_08815_b200 import network as nw
+    from paper_2212_08815_b200.sparse_core import prune_random
+
+    g = load_golden("pipeline.npz")
+    for i in range(int(g["n_net_cases"])):
+        key = f"net{i}"
+        kind, variant, seed = str(g[f"{key}__kind"]), str(g[f"{key}__variant"]), int(g[f"{key}__seed"])
+        net = nw.build_benchmark_net(kind, 0.125, input_hw=32, variant=variant)
+        weights = nw.random_weights(net, seed)
+        if variant == "sparse_filter":
+            weights = nw.prune_weights(weights, 0.3, seed)
+        assert weights_sha(weights) == str(g[f"{key}__weights_sha"]), key
+        x = prune_random(nw.random_input(net.input_dims, seed), 0.4, seed)
+        assert x.to_array().tobytes() == g[f"{key}__x"].tobytes(), key

@@ -1,0 +1,153 @@
+"""The sparse-input pipeline and the remaining layer operators on the GPU (SURVEY.md
+§8f-1 and §8f-2), bit-exact against the reference's own outputs
+(tests/golden/pipeline.npz, made by tests/golden/make_golden.py::gen_pipeline):
+
+* node-format ReLU / LeakyReLU (rebuild_tensor3 semantics, incl. explicit +0.0 / -0.0 /
+  NaN nodes), pool_sparse, batch norm, pad (CHW node pad keeps explicit zero nodes),
+  all six axis orders;
+* the dense baseline conv (layer and single filter) and dot_dense_sparse;
+* transpose_matrix / transpose_tensor3 (values move untouched);
+* prepare/forward of the sparse_input, dense_baseline and sparse_filter variants on
+  the desk-scale VGG16 and YOLO stacks (incl. the conv+pool fusion rule and per-layer
+  density recording), random_weights / prune_weights / prune_random, and
+  density_evolution.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, nodes_from_i64, weights_sha
+
+import paper_2212_08815_b200 as fs
+from paper_2212_08815_b200 import network as nw
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    return load_golden("pipeline.npz")
+
+
+def _sparse(g, key):
+    return fs.SparseTensor3(fs.AxisOrder3[str(g[f"{key}__order"])], tuple(int(v) for v in g[f"{key}__dims"]),
+                            nodes_from_i64(g[f"{key}__nodes"]), g[f"{key}__matrix_offsets"],
+                            g[f"{key}__segment_offsets"])
+
+
+def _same_sparse(t, g, key):
+    assert t.order.name == str(g[f"{key}__order"]), key
+    assert tuple(t.dims) == tuple(int(v) for v in g[f"{key}__dims"]), key
+    assert np.ascontiguousarray(t.nodes).view(np.int64).tobytes() == g[f"{key}__nodes"].tobytes(), key
+    assert np.array_equal(np.asarray(t.segment_offsets, np.int64), g[f"{key}__segment_offsets"]), key
+    assert np.array_equal(np.asarray(t.matrix_offsets, np.int64), g[f"{key}__matrix_offsets"]), key
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.int32)
+
+
+def test_node_format_activation_pool_batchnorm_pad(g):
+    for i in range(int(g["n_node_cases"])):
+        key = f"n{i}"
+        t = _sparse(g, f"{key}_in")
+        _same_sparse(fs.apply_activation(t, "relu"), g, f"{key}_relu")
+        _same_sparse(fs.apply_activation(t, "leaky_relu", 0.1), g, f"{key}_leaky")
+        _same_sparse(fs.pool_sparse(t, (2, 2), str(g[f"{key}_pool__mode"])), g, f"{key}_pool")
+        _same_sparse(fs.pad_tensor(t, int(g[f"{key}_pad__p"])), g, f"{key}_pad")
+        bn = fs.BatchNormParams(scale=g[f"{key}_bn__scale"], shift=g[f"{key}_bn__shift"],
+                                mean=g[f"{key}_bn__mean"], var=g[f"{key}_bn__var"], epsilon=1e-5)
+        _same_sparse(fs.apply_batchnorm(t, bn), g, f"{key}_bn")
+        d = fs.DenseTensor3.from_array(g[f"{key}_dense__x"])
+        assert np.array_equal(_bits(fs.apply_batchnorm(d, bn).to_array()), _bits(g[f"{key}_dense_bn__y"])), key
+        assert np.array_equal(_bits(fs.apply_activation(d, "leaky_relu", 0.1).to_array()),
+                              _bits(g[f"{key}_dense_leaky__y"])), key
+        assert np.array_equal(_bits(fs.pad_tensor(d, int(g[f"{key}_pad__p"])).to_array()),
+                              _bits(g[f"{key}_dense_pad__y"])), key
+
+
+def test_layer_op_validation_messages():
+    t = fs.sparsify_tensor3(fs.DenseTensor3.from_array(np.ones((2, 4, 4), np.float32)), fs.AxisOrder3.CHW)
+    with pytest.raises(ValueError, match="divisible"):
+        fs.pool_sparse(t, (3, 3), "max")
+    with pytest.raises(ValueError, match="positive"):
+        fs.pool_sparse(t, (0, 2), "max")
+    with pytest.raises(ValueError, match="non-negative"):
+        fs.pad_tensor(t, -1)
+    assert fs.pad_tensor(t, 0) is t
+    with pytest.raises(ValueError, match="slope"):
+        fs.apply_activation(t, "leaky_relu", -0.1)
+    with pytest.raises(ValueError, match="shape"):
+        fs.apply_batchnorm(t, fs.BatchNormParams(np.ones(3), np.zeros(3), np.zeros(3), np.ones(3)))
+    with pytest.raises(fs.FormatError, match="WHC"):
+        fs.transpose_tensor3(t)
+
+
+def test_dense_baseline_conv_bitwise(g):
+    for i in range(int(g["n_dense_cases"])):
+        x, w, bias = g[f"d{i}__x"], g[f"d{i}__w"], g[f"d{i}__bias"]
+        s, p = (int(v) for v in g[f"d{i}__geom"])
+        t_in = fs.DenseTensor3.from_array(x)
+        y = fs.conv_forward_dense(t_in, [fs.DenseTensor3.from_array(f) for f in w], s, p, bias)
+        assert np.array_equal(_bits(y.to_array()), _bits(g[f"d{i}__y"])), i
+        geom = fs.ConvGeometry(tuple(x.shape), tuple(w.shape[1:]), s, p)
+        y0 = fs.dense_conv_reference(t_in, fs.DenseTensor3.from_array(w[0]), geom)
+        assert np.array_equal(_bits(y0), _bits(g[f"d{i}__y0"])), i
+
+
+def test_dot_dense_sparse_bitwise(g):
+    for i in range(6):
+        sv = fs.SparseVector(int(g[f"dot{i}__length"]), nodes_from_i64(g[f"dot{i}__nodes"]))
+        got = fs.dot_dense_sparse(g[f"dot{i}__d"], sv)
+        assert np.float32(got).tobytes() == np.float32(g[f"dot{i}__y"]).tobytes(), i
+
+
+def test_transposes_move_nodes_untouched(g):
+    for i in range(6):
+        m = fs.SparseMatrix(fs.AxisOrder2[str(g[f"tm{i}_in__order"])], *(int(v) for v in g[f"tm{i}_in__shape"]),
+                            nodes_from_i64(g[f"tm{i}_in__nodes"]), g[f"tm{i}_in__segment_offsets"])
+        mt = fs.transpose_matrix(m)
+        assert mt.order.name == str(g[f"tm{i}_out__order"])
+        assert np.ascontiguousarray(mt.nodes).view(np.int64).tobytes() == g[f"tm{i}_out__nodes"].tobytes(), i
+        assert np.array_equal(np.asarray(mt.segment_offsets, np.int64), g[f"tm{i}_out__segment_offsets"]), i
+        # and back: the round trip restores the input exactly
+        back = fs.transpose_matrix(mt)
+        assert np.ascontiguousarray(back.nodes).view(np.int64).tobytes() == g[f"tm{i}_in__nodes"].tobytes(), i
+    for i in range(4):
+        _same_sparse(fs.transpose_tensor3(_sparse(g, f"tt{i}_in")), g, f"tt{i}_out")
+
+
+def test_network_variants_bitwise(g):
+    fs.set_exact(True)  # the sparse_filter variant's bit-exact kernel
+    try:
+        for i in range(int(g["n_net_cases"])):
+            key = f"net{i}"
+            kind, variant, seed = str(g[f"{key}__kind"]), str(g[f"{key}__variant"]), int(g[f"{key}__seed"])
+            net = nw.build_benchmark_net(kind, 0.125, input_hw=32, variant=variant)
+            weights = nw.random_weights(net, seed)
+            if variant == "sparse_filter":
+                weights = nw.prune_weights(weights, 0.3, seed)
+            assert weights_sha(weights) == str(g[f"{key}__weights_sha"]), key
+            x = fs.prune_random(nw.random_input(net.input_dims, seed), 0.4, seed)
+            assert np.array_equal(_bits(x.to_array()), _bits(g[f"{key}__x"])), key
+            inp = fs.sparsify_tensor3(x, fs.AxisOrder3.CHW) if variant == "sparse_input" else x
+            res = nw.forward(nw.prepare(net, weights), [inp], record_density=True)
+            out = res.outputs[0]
+            if isinstance(out, fs.SparseTensor3):
+                _same_sparse(out, g, f"{key}_out")
+            else:
+                assert np.array_equal(_bits(out.to_array()), _bits(g[f"{key}_out__y"])), key
+            assert np.array_equal(np.array(res.report.layer_densities, np.float64), g[f"{key}__densities"]), key
+    finally:
+        fs.set_exact(False)
+
+
+def test_density_evolution_matches_reference(g):
+    net = nw.build_benchmark_net("vgg16_desk", 0.125, input_hw=32, variant="sparse_input")
+    recs = nw.density_evolution(net, [0.1, 0.5, 1.0], 2020)
+    assert [r.input_density for r in recs] == list(g["evo__input"])
+    assert [r.layer_index for r in recs] == list(g["evo__layer"])
+    assert [r.layer_kind for r in recs] == [str(k) for k in g["evo__kind"]]
+    assert np.array_equal(np.array([r.output_density for r in recs]), g["evo__density"])
+    with pytest.raises(ValueError, match="sparse_input"):
+        nw.density_evolution(net.with_variant("dense_baseline"), [0.5], 1)
