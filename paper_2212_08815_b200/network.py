@@ -20,6 +20,7 @@ layers.py, exactly following the reference's step logic (network.py:410-461).
 from __future__ import annotations
 
 import math
+import struct
 import time
 from dataclasses import dataclass, replace
 
@@ -29,8 +30,11 @@ from . import layers as ly
 from .sparse_core import (
     AxisOrder3,
     DenseTensor3,
+    FormatError,
     SparseTensor3,
     SparseTensor4,
+    dense3_from_bytes,
+    dense3_to_bytes,
     density,
 )
 
@@ -40,6 +44,8 @@ VARIANT_DENSE = "dense_baseline"
 VARIANTS = (VARIANT_SPARSE_FILTER, VARIANT_SPARSE_INPUT, VARIANT_DENSE)
 
 BENCH_KINDS = ("vgg16_desk", "yolo_desk", "vgg16_desk_noact", "yolo_desk_nobn")
+WEIGHT_MAGIC = b"FSNW"
+WEIGHT_VERSION = 1
 _VGG16_PLAN = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
 _YOLO_BLOCKS = [16, 32, 64, 128, 256]
 _YOLO_HEAD = [512, 256]
@@ -469,3 +475,151 @@ def density_evolution(net: NetworkSpec, input_density_sweep: list, seed: int) ->
         for li, layer in enumerate(net.layers):
             records.append(DensityRecord(d, li + 1, layer.kind, result.report.layer_densities[li]))
     return records
+
+
+# -- model text and FSNW weight files (network.py:99-167, :210-294): host-side I/O -------
+
+
+def parse_model_text(text: str, name: str = "model") -> NetworkSpec:
+    """Line-oriented model format: ``input c= h= w=`` then one layer per line
+    (conv out= k= [s=] [p=], maxpool/avgpool k=, relu, leaky_relu slope=, batchnorm,
+    pad p=); '#' starts a comment."""
+    dims, stack = None, []
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        kind, *fields = line.split()
+        args = {}
+        for f in fields:
+            key, sep, val = f.partition("=")
+            if not sep:
+                raise FormatError(f"line {lineno}: malformed key=value field")
+            args[key] = val
+        try:
+            if kind == "input":
+                dims = (int(args["c"]), int(args["h"]), int(args["w"]))
+            elif kind == "conv":
+                k = int(args["k"])
+                stack.append(ly.LayerSpec(kind="conv", out_channels=int(args["out"]), kernel=(k, k),
+                                          stride=int(args.get("s", 1)), padding=int(args.get("p", 0))))
+            elif kind in ("maxpool", "avgpool"):
+                k = int(args["k"])
+                stack.append(ly.LayerSpec(kind=kind, kernel=(k, k)))
+            elif kind in ("relu", "batchnorm"):
+                stack.append(ly.LayerSpec(kind=kind))
+            elif kind == "leaky_relu":
+                stack.append(ly.LayerSpec(kind="leaky_relu", slope=float(args["slope"])))
+            elif kind == "pad":
+                stack.append(ly.LayerSpec(kind="pad", padding=int(args["p"])))
+            else:
+                raise FormatError(f"line {lineno}: unknown layer kind {kind!r}")
+        except (KeyError, ValueError) as e:
+            raise FormatError(f"line {lineno}: {e}") from None
+    if dims is None:
+        raise FormatError("model text is missing an 'input c= h= w=' line")
+    net = NetworkSpec(name=name, input_dims=dims, layers=stack)
+    net.shape_chain()
+    return net
+
+
+def format_model_text(net: NetworkSpec) -> str:
+    c, h, w = net.input_dims
+    out = [f"input c={c} h={h} w={w}"]
+    for l in net.layers:
+        if l.kind == "conv":
+            out.append(f"conv out={l.out_channels} k={l.kernel[0]} s={l.stride} p={l.padding}")
+        elif l.kind in ("maxpool", "avgpool"):
+            out.append(f"{l.kind} k={l.kernel[0]}")
+        elif l.kind == "leaky_relu":
+            out.append(f"leaky_relu slope={l.slope:g}")
+        elif l.kind == "pad":
+            out.append(f"pad p={l.padding}")
+        else:
+            out.append(l.kind)
+    return "\n".join(out) + "\n"
+
+
+def save_weights(path, net: NetworkSpec, weights: NetworkWeights) -> None:
+    """FSNW file: magic, u32 version, u32 entry count, then per parameterized layer --
+    conv: u32 K, C, H_F, W_F, K FDT3 filter blobs, K f32 biases; batchnorm: C f32 each of
+    scale, shift, mean, var, then f32 epsilon (little endian)."""
+    params = parameterized_layers(net)
+    if len(params) != len(weights.entries):
+        raise ValueError(f"{len(weights.entries)} entries for {len(params)} parameterized layers")
+    blob = bytearray(WEIGHT_MAGIC + struct.pack("<II", WEIGHT_VERSION, len(params)))
+    for (_, layer), entry in zip(params, weights.entries):
+        if layer.kind == "conv":
+            filters = np.asarray(entry.filters, np.float32)
+            blob += struct.pack("<IIII", *filters.shape)
+            for f in filters:
+                blob += dense3_to_bytes(DenseTensor3.from_array(f))
+            blob += np.asarray(entry.bias, dtype="<f4").tobytes()
+        else:
+            for arr in (entry.scale, entry.shift, entry.mean, entry.var):
+                blob += np.asarray(arr, dtype="<f4").tobytes()
+            blob += struct.pack("<f", entry.epsilon)
+    with open(path, "wb") as fh:
+        fh.write(bytes(blob))
+
+
+def load_weights(path, net: NetworkSpec) -> NetworkWeights:
+    """Read an FSNW file and validate it against the layer stack (same messages as the
+    reference: magic, version, entry count, dims, truncation, trailing bytes)."""
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if raw[:4] != WEIGHT_MAGIC:
+        raise FormatError(f"bad magic {raw[:4]!r}, expected {WEIGHT_MAGIC!r}")
+    if len(raw) < 12:
+        raise FormatError("truncated weight file header")
+    version, count = struct.unpack_from("<II", raw, 4)
+    if version != WEIGHT_VERSION:
+        raise FormatError(f"unsupported weight file version {version}")
+    params = parameterized_layers(net)
+    if count != len(params):
+        raise FormatError(f"weight file has {count} parameterized layers, network expects {len(params)}")
+    chain = [net.input_dims] + net.shape_chain()
+    at = 12
+    entries = []
+
+    def need(n, where):
+        if at + n > len(raw):
+            raise FormatError(f"truncated weight file in {where}")
+
+    for li, layer in params:
+        where = f"layer {li} ({layer.kind})"
+        if layer.kind == "conv":
+            need(16, where)
+            dims = struct.unpack_from("<IIII", raw, at)
+            at += 16
+            expect = (layer.out_channels, chain[li][0]) + tuple(layer.kernel)
+            if tuple(dims) != expect:
+                raise FormatError(f"filter dims {tuple(dims)} != {expect} in {where}")
+            k, c, h, w = dims
+            per = 16 + 4 * c * h * w
+            filters = np.empty(dims, np.float32)
+            for f in range(k):
+                need(per, where)
+                t = dense3_from_bytes(raw[at:at + per])
+                if tuple(t.dims) != (c, h, w):
+                    raise FormatError(f"filter {f} dims {t.dims} != {(c, h, w)} in {where}")
+                filters[f] = t.to_array()
+                at += per
+            need(4 * k, where)
+            bias = np.frombuffer(raw, dtype="<f4", count=k, offset=at).astype(np.float32)
+            at += 4 * k
+            entries.append(ConvParams(filters=filters, bias=bias))
+        else:
+            c_in = chain[li][0]
+            need(16 * c_in + 4, where)
+            stats = []
+            for _ in range(4):
+                stats.append(np.frombuffer(raw, dtype="<f4", count=c_in, offset=at).astype(np.float32))
+                at += 4 * c_in
+            (eps,) = struct.unpack_from("<f", raw, at)
+            at += 4
+            entries.append(ly.BatchNormParams(scale=stats[0], shift=stats[1], mean=stats[2], var=stats[3],
+                                              epsilon=float(eps)))
+    if at != len(raw):
+        raise FormatError(f"{len(raw) - at} trailing bytes after last layer")
+    return NetworkWeights(entries=entries)

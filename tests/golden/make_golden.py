@@ -393,7 +393,43 @@ def gen_pipeline(out):
     np.savez_compressed(os.path.join(out, "pipeline.npz"), **payload)
 
 
+def gen_formats(out):
+    """The reference's on-disk formats: FSCT / FDT3 tensor blobs, FSNW
+    weight files and the model text format, byte for byte."""
+    import tempfile
+
+    rng = np.random.default_rng(2009)
+    payload = {}
+    for i, o in enumerate(si.AxisOrder3):
+        dims = tuple(int(v) for v in rng.integers(1, 6, 3))
+        x = rand_input(rng, dims, 0.5)
+        t = si.sparsify_tensor3(si.DenseTensor3.from_array(x), o)
+        payload[f"t{i}__x"] = x
+        payload[f"t{i}__order"] = np.array(o.name)
+        payload[f"t{i}__fsct"] = np.frombuffer(si.sparse3_to_bytes(t), np.uint8)
+        payload[f"t{i}__fdt3"] = np.frombuffer(si.dense3_to_bytes(si.DenseTensor3.from_array(x)), np.uint8)
+    texts = [nw.format_model_text(nw.build_benchmark_net(kind, 0.125, input_hw=32)) for kind in nw.BENCH_KINDS]
+    for j, kind in enumerate(("yolo_desk", "vgg16_desk")):
+        net = nw.build_benchmark_net(kind, 0.0625, input_hw=32)
+        w = nw.random_weights(net, 2010 + j)
+        with tempfile.NamedTemporaryFile(suffix=".fsnw", delete=False) as fh:
+            path = fh.name
+        nw.save_weights(path, net, w)
+        payload[f"w{j}__kind"] = np.array(kind)
+        payload[f"w{j}__sha"] = np.array(sha(*[np.asarray(getattr(e, a)) for e in w.entries
+                                               for a in (("filters", "bias") if hasattr(e, "filters")
+                                                         else ("scale", "shift", "mean", "var"))]))
+        payload[f"w{j}__fsnw"] = np.fromfile(path, np.uint8)
+        os.unlink(path)
+    payload["model_texts"] = np.array(texts)
+    custom = "# a test stack\ninput c=3 h=14 w=14\nconv out=8 k=3 s=1 p=1  # first\nbatchnorm\nleaky_relu slope=0.1\npad p=1\nmaxpool k=2\nconv out=4 k=3 p=1\navgpool k=2\nrelu\n"
+    payload["custom_text"] = np.array(custom)
+    payload["custom_formatted"] = np.array(nw.format_model_text(nw.parse_model_text(custom, "custom")))
+    np.savez_compressed(os.path.join(out, "formats.npz"), **payload)
+
+
 def main():
+    gen_formats(HERE)
     gen_pipeline(HERE)
     gen_encoder(HERE)
     gen_sf(HERE)
