@@ -428,7 +428,29 @@ def gen_formats(out):
     np.savez_compressed(os.path.join(out, "formats.npz"), **payload)
 
 
+def gen_harness(out):
+    """The reference harness's density outputs (bench_cli.run_bench's probe rows and
+    run_density_study) for small configs; timings are machine-specific and not kept."""
+    from sparse_infer import bench_cli as bc
+
+    payload = {}
+    for i, (kind, variant) in enumerate((("vgg16_desk", "sparse_input"), ("vgg16_desk", "sparse_filter"))):
+        cfg = bc.BenchConfig(net_kind=kind, scale=0.125, variant=variant, densities=[0.1, 0.5], reps=3,
+                             timing_csv=None, density_csv=None)
+        timing, dens = bc.run_bench(cfg)
+        payload[f"b{i}__kind"], payload[f"b{i}__variant"] = np.array(kind), np.array(variant)
+        payload[f"b{i}__timing_keys"] = np.array([f"{r.variant}|{r.density:g}|{r.batch}|{r.workers}|{r.strategy}|{r.rep}"
+                                                  for r in timing])
+        payload[f"b{i}__density"] = np.array([[r.input_density, r.layer_index, r.output_density] for r in dens])
+        payload[f"b{i}__density_kind"] = np.array([r.layer_kind for r in dens])
+    cfg = bc.BenchConfig(net_kind="yolo_desk", scale=0.125, variant="sparse_input", densities=[0.2, 1.0], reps=3)
+    for kind, rows in bc.run_density_study(cfg).items():
+        payload[f"study_{kind}"] = np.array([[r.input_density, r.layer_index, r.output_density] for r in rows])
+    np.savez_compressed(os.path.join(out, "harness.npz"), **payload)
+
+
 def main():
+    gen_harness(HERE)
     gen_formats(HERE)
     gen_pipeline(HERE)
     gen_encoder(HERE)
