@@ -6,25 +6,23 @@
 //    nodes ascending c; __fmul_rn + __fadd_rn (no contraction, like numba).
 //    Any geometry.  Reads the reference's CHW node buffer directly.
 //
-// 2) sf3x3_kernel -- the fast path for 3x3/s1/p1 (all VGG16 convs).  GEMM-like
-//    "dense activations x unstructured-sparse filters" on FP32 CUDA cores:
-//      * a CTA owns LI rectangular sub-regions of (4*LY) x 16 output pixels (LY*LI = 8)
-//        and 64 output channels; warp w owns filter group g (8 filters);
-//      * lane = one 4x4 output tile; it keeps acc[8 filters][4][4] in registers;
-//      * input channels stream through shared memory in chunks of CC channels: one
-//        TMA box per sub-region per chunk ((4LY+2) x 20 floats x CC, zero fill for
-//        the conv padding) plus a bulk copy of each warp's packed nonzero list for
-//        those channels, completed on an mbarrier (S-stage ring).  There is no
-//        producer warp: each warp restages its own entry run as soon as it leaves a
-//        stage, and the last warp to leave (smem counter) restages the shared boxes,
-//        so warps drift freely within the ring instead of waiting for a producer;
-//      * per channel a lane loads its 6x6 input patch into registers (12 x LDS.128,
-//        conflict-free with the 20-float row pitch), then walks the warp-uniform
-//        nonzero list (kl, tap, value); a switch dispatches each nonzero to 16
-//        statically indexed FFMAs -- every loaded input value is reused by all
-//        nonzeros of that channel (~0.9 * 8 of them at 90% sparsity);
-//      * epilogue: + bias, optional ReLU, optional fused 2x2 max-pool (the
-//        reference's relu -> pool order, -inf start, '>' compare), float4 stores.
+// 2) sf3x3_kernel -- the fast path for 3x3/s1/p1 (all VGG16 convs).  Dense activations x
+//    unstructured-sparse filters on FP32 CUDA cores:
+//      * a CTA owns 32 lane tiles (LI sub-regions of (4*LY) x 16 output pixels, LY*LI = 8)
+//        and 32 output channels; warp w owns filter group g (KT = 4 filters);
+//      * lane = one 4x4 output tile; acc[KT][4][4] in registers as FFMA2 column pairs;
+//      * input channels stream through shared memory in chunks of CC channels: one TMA
+//        box per sub-region per chunk ((4LY+2) x 20 floats x CC, zero fill for the conv
+//        padding) plus a bulk copy of each warp's packed nonzero list, completed on an
+//        mbarrier (S-stage ring).  No producer warp: each warp restages its own entry
+//        run as soon as it leaves a stage, and the last warp to leave (smem counter)
+//        restages the shared boxes, so warps drift freely within the ring;
+//      * per channel a lane loads its 6x6 input patch into registers, then walks the
+//        warp-uniform nonzero list through a jump table (sf3x3_dispatch.inc, generated
+//        by gen_sf3x3_dispatch.py): each nonzero is 8 FFMA2 / 16 FFMA on statically
+//        named registers, every loaded input value reused by all nonzeros of the channel;
+//      * epilogue: + bias, optional ReLU, optional fused 2x2 max-pool (the reference's
+//        relu -> pool order, -inf start, '>' compare).
 #include <cuda.h>
 #include <stdlib.h>
 
