@@ -227,6 +227,13 @@ int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_n
                       void *stream);
 int fscnn_nchw_to_whc(const float *x_nchw, int n, int c, int h, int w, float *y_whc,
                       void *stream);
+/* Pitched variants: the NCHW side has row pitch ld (floats) and its rows start at column
+ * col0 -- (ld, col0) = (halo_pitch(w), 1) reads/writes the fast kernel's halo-column
+ * layout directly, so the public-API forward stages and unstages in one pass each. */
+int fscnn_whc_to_nchw_ex(const float *x_whc, int n, int c, int h, int w, float *y, int ld,
+                         int col0, void *stream);
+int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int col0, float *y_whc,
+                         void *stream);
 
 /* FP32 CUDA-core throughput probe (roofline denominator): `blocks` x 256 threads,
  * each 8 independent FFMA chains of 16*iters steps = 256*blocks*iters*256 FLOPs. */

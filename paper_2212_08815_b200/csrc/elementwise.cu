@@ -130,13 +130,15 @@ __global__ void maxpool2x2_kernel(const float *__restrict__ x, int64_t total, in
     }
 }
 
-// (W,H,C)-memory image -> NCHW, 32x32 smem transpose over (c, hw) per image.
+// (W,H,C)-memory image -> NCHW, 32x32 smem transpose over (c, hw) per image.  The NCHW
+// side has row pitch ld and starts at column col0 (ld = w, col0 = 0: dense; the halo
+// layout of the fast kernel: ld = halo pitch, col0 = 1).
 __global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
-                                   float *__restrict__ y) {
+                                   int ld, int col0, float *__restrict__ y) {
     __shared__ float tile[32][33];
     int img = blockIdx.z;
     const float *src = x + (int64_t)img * c_n * hw;
-    float *dst = y + (int64_t)img * c_n * hw;
+    float *dst = y + (int64_t)img * c_n * h * ld + col0;
     int c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;  // p = w*H + h in source order
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         int p = p0 + j, c = c0 + threadIdx.x;
@@ -147,21 +149,21 @@ __global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw,
         int c = c0 + j, p = p0 + threadIdx.x;
         if (p < hw && c < c_n) {
             int wi = p / h, hi = p % h;
-            dst[(int64_t)c * hw + (int64_t)hi * w + wi] = tile[threadIdx.x][j];
+            dst[((int64_t)c * h + hi) * ld + wi] = tile[threadIdx.x][j];
         }
     }
 }
 
 __global__ void nchw_to_whc_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
-                                   float *__restrict__ y) {
+                                   int ld, int col0, float *__restrict__ y) {
     __shared__ float tile[32][33];
     int img = blockIdx.z;
-    const float *src = x + (int64_t)img * c_n * hw;
+    const float *src = x + (int64_t)img * c_n * h * ld + col0;
     float *dst = y + (int64_t)img * c_n * hw;
     int c0 = blockIdx.y * 32, q0 = blockIdx.x * 32;  // q = h*W + w in source order
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
         int c = c0 + j, q = q0 + threadIdx.x;
-        if (q < hw && c < c_n) tile[j][threadIdx.x] = src[(int64_t)c * hw + q];
+        if (q < hw && c < c_n) tile[j][threadIdx.x] = src[((int64_t)c * h + q / w) * ld + q % w];
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -263,24 +265,36 @@ int fscnn_pool2d(const float *x, int n, int c, int h, int w, int h_p, int w_p, i
     return FSCNN_OK;
 }
 
-int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_nchw,
-                      void *stream) {
+int fscnn_whc_to_nchw_ex(const float *x_whc, int n, int c, int h, int w, float *y, int ld,
+                         int col0, void *stream) {
     FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    FSCNN_REQUIRE(col0 >= 0 && ld >= w + col0, "row pitch too small");
     if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
     dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
-    whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, y_nchw);
+    whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, ld, col0, y);
     FSCNN_LAUNCH_CHECK("whc_to_nchw_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_whc_to_nchw(const float *x_whc, int n, int c, int h, int w, float *y_nchw,
+                      void *stream) {
+    return fscnn_whc_to_nchw_ex(x_whc, n, c, h, w, y_nchw, w, 0, stream);
+}
+
+int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int col0, float *y_whc,
+                         void *stream) {
+    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
+    FSCNN_REQUIRE(col0 >= 0 && ld >= w + col0, "row pitch too small");
+    if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
+    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
+    nchw_to_whc_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x, c, h * w, h, w, ld, col0, y_whc);
+    FSCNN_LAUNCH_CHECK("nchw_to_whc_kernel");
     return FSCNN_OK;
 }
 
 int fscnn_nchw_to_whc(const float *x_nchw, int n, int c, int h, int w, float *y_whc,
                       void *stream) {
-    FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
-    if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
-    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
-    nchw_to_whc_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_nchw, c, h * w, h, w, y_whc);
-    FSCNN_LAUNCH_CHECK("nchw_to_whc_kernel");
-    return FSCNN_OK;
+    return fscnn_nchw_to_whc_ex(x_nchw, n, c, h, w, w, 0, y_whc, stream);
 }
 
 int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w_crsk,

@@ -466,6 +466,23 @@ def whc_to_nchw(x_whc: torch.Tensor, n: int, c: int, h: int, w: int, out=None) -
     return out
 
 
+def whc_to_halo(x_whc: torch.Tensor, n: int, c: int, h: int, w: int, out: torch.Tensor) -> torch.Tensor:
+    """(W,H,C)-memory images straight into a halo-column buffer [N, C, H, pitch]."""
+    assert out.is_contiguous() and tuple(out.shape[:3]) == (n, c, h) and out.shape[3] >= w + 1
+    call("fscnn_whc_to_nchw_ex", ptr(x_whc), n, c, h, w, ptr(out), int(out.shape[3]), 1, stream())
+    return out
+
+
+def halo_to_whc(xh: torch.Tensor, w: int, out=None) -> torch.Tensor:
+    """Logical [N, C, H, w] of a halo-column buffer -> (W,H,C)-memory images [N, W, H, C]."""
+    assert xh.is_contiguous()
+    n, c, h, ld = (int(v) for v in xh.shape)
+    if out is None:
+        out = torch.empty((n, w, h, c), dtype=torch.float32, device=xh.device)
+    call("fscnn_nchw_to_whc_ex", ptr(xh), n, c, h, w, ld, 1, ptr(out), stream())
+    return out
+
+
 def nchw_to_whc(x: torch.Tensor, out=None) -> torch.Tensor:
     x = x.contiguous()
     n, c, h, w = (int(v) for v in x.shape)

@@ -123,6 +123,14 @@ class VGGEngine:
             w = w // 2 if st.pool else w
         return cur
 
+    def forward_whc(self, x_whc: torch.Tensor, n: int) -> torch.Tensor:
+        """Device (W,H,C)-memory images (the reference's DenseTensor3 payloads, n of them
+        back to back) -> device (W,H,C) outputs [n, W', H', 512]: the input is written
+        straight into the halo buffer and the output read straight out of it."""
+        bufs = self._buffers(n)
+        device.whc_to_halo(x_whc, n, self.in_c, self.hw, self.hw, self._in)
+        return device.halo_to_whc(self.run(self._in), self.out_hw)
+
     def forward_device(self, x: torch.Tensor) -> torch.Tensor:
         """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer)."""
         assert x.shape[1] == self.in_c and x.shape[2] == self.hw and x.shape[3] == self.hw

@@ -215,6 +215,24 @@ def test_worker_strategy_and_batch_invariance_bitwise():
         assert fs.forward(prepared, [xs[i]]).outputs[0].data.tobytes() == ref[i]
 
 
+def test_pinned_batch_forward_equals_pageable():
+    """network.pinned_batch inputs take the zero-copy DMA path; results are identical to
+    the packed pageable path, including for a sub-list and a reordered list."""
+    g, net, weights = _small_vgg()
+    prepared = fs.prepare(net, weights)
+    rng = np.random.default_rng(87)
+    arrs = [rng.standard_normal((3, 32, 32)).astype(np.float32) for _ in range(5)]
+    pageable = [fs.DenseTensor3.from_array(a) for a in arrs]
+    pinned = fs.pinned_batch(5, (3, 32, 32))
+    for t, a in zip(pinned, arrs):
+        t.data[:] = fs.DenseTensor3.from_array(a).data
+    ref = [o.data.tobytes() for o in fs.forward(prepared, pageable).outputs]
+    assert [o.data.tobytes() for o in fs.forward(prepared, pinned).outputs] == ref
+    assert [o.data.tobytes() for o in fs.forward(prepared, pinned[:3]).outputs] == ref[:3]
+    rev = pinned[::-1]  # not back to back in memory -> packed path, same results
+    assert [o.data.tobytes() for o in fs.forward(prepared, rev).outputs] == ref[::-1]
+
+
 def test_forward_rejects_mismatches():
     g, net, weights = _small_vgg()
     p = fs.prepare(net, weights)
