@@ -148,12 +148,22 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
     FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
     if (n == 0 || k == 0) return FSCNN_OK;
     FSCNN_REQUIRE(in_nodes && in_seg_off && wq && y, "null buffer");
-    constexpr int S = 8;
+    // Strip width: 8 outputs per warp reuse each node for up to three of them, but a
+    // small problem (one image, as the per-image layer API runs) then fills only a few
+    // SMs; halve the strip until about 24 warps per SM are busy (2 outputs minimum).
+    const int64_t k_blocks = ceil_div(k, 32);
+    auto warps_for = [&](int s_) { return (int64_t)n * h * ceil_div(w, s_) * k_blocks; };
+    const int S = warps_for(8) >= 148 * 24 ? 8 : (warps_for(4) >= 148 * 24 ? 4 : 2);
     const int strips = (int)ceil_div(w, S);
-    dim3 grid((unsigned)ceil_div((int64_t)h * strips, 4), (unsigned)ceil_div(k, 32), (unsigned)n);
-    si_strip_kernel<S><<<grid, 128, 0, as_stream(stream)>>>(
-        reinterpret_cast<const int2 *>(in_nodes), in_seg_off, c, h, w,
-        reinterpret_cast<const float4 *>(wq), k, strips, bias, y);
+    dim3 grid((unsigned)ceil_div((int64_t)h * strips, 4), (unsigned)k_blocks, (unsigned)n);
+    auto args = [&](auto kern) {
+        kern<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const int2 *>(in_nodes), in_seg_off, c,
+                                                   h, w, reinterpret_cast<const float4 *>(wq), k, strips,
+                                                   bias, y);
+    };
+    if (S == 8) args(si_strip_kernel<8>);
+    else if (S == 4) args(si_strip_kernel<4>);
+    else args(si_strip_kernel<2>);
     FSCNN_LAUNCH_CHECK("si_strip_kernel");
     return FSCNN_OK;
 }

@@ -5,10 +5,10 @@ layers.py:302-323) are the same GPU launch here: all filters of the layer in one
 kernel.  Their results are therefore bit-identical, as the reference guarantees, and
 independent of ``workers`` (accepted for API compatibility; layers.py:149-155).
 
-Kernel choice: 3x3 / stride 1 / pad 1 layers use the fast channel-major kernel
-(fp32 reassociation, held to 1e-4 normwise); any other geometry -- or
-``set_exact(True)`` / FSCNN_EXACT=1 -- uses the reference-order kernel, bit-exact with
-the reference.
+Kernel choice: 3x3 / stride 1 / pad 1 layers big enough to fill the GPU use the fast
+channel-major kernel (fp32 reassociation, held to 1e-4 normwise); smaller ones (one
+56x56 image, as config 1), any other geometry, or ``set_exact(True)`` / FSCNN_EXACT=1
+use the reference-order kernel, bit-exact with the reference.
 """
 
 from __future__ import annotations
@@ -126,6 +126,19 @@ def _device_bank(filters: SparseTensor4):
     return entry
 
 
+def _fast_fills_gpu(dims, k: int) -> bool:
+    """The tiled fast kernel gives each CTA 512 outputs x 32 filters; for one small image
+    (BASELINE config 1: 56x56, 64 filters -> 16 CTAs) it leaves most of the 148 SMs idle
+    and the reference-order kernel (one thread per output and filter) is faster
+    (measured 13 vs 22 us, profiles/r01_configs_12.json) -- and bit-exact."""
+    from . import device
+
+    c, h, w = dims
+    ly = device.pick_ly(c, h)
+    units = -(-(-(-h // (4 * ly)) * -(-w // 16)) // (8 // ly))
+    return units * -(-k // device.CTA_FILTERS) >= 148
+
+
 def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: int, bias) -> DenseTensor3:
     import torch
 
@@ -138,7 +151,7 @@ def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: 
     nodes, seg, packed = _device_bank(filters)
     b = torch.from_numpy(np.ascontiguousarray(bias, dtype=np.float32)).cuda()
     x = kernels.dense_to_device(t_in)
-    if packed is not None and stride == 1 and padding == 1 and not _EXACT:
+    if packed is not None and stride == 1 and padding == 1 and not _EXACT and _fast_fills_gpu(t_in.dims, k):
         c, h, w = t_in.dims
         y = device.sf_conv3x3(device.to_halo(x), packed, b, relu=False, pool=False, w=w)
         y = device.from_halo(y, w).contiguous()
