@@ -341,16 +341,22 @@ constexpr int kSfPackKt = 4;  // default filters per group (sf_conv.cu supports 
 
 // Fast-stream marking: the last nonzero of every (group, channel) segment gets
 // index + kt*9 (its jump-table variant that falls into the channel transition);
-// an empty segment's sentinel slot becomes index 2*kt*9 (transition without FMAs).
-// Other sentinel slots are skipped by the kernel and never dispatched.
+// an empty segment's sentinel slot becomes (2*kt*9, run) where run >= 1 counts the
+// consecutive empty segments starting at it (the kernel skips a run with one dispatch,
+// clipping it to the channel chunk).  Other sentinel slots are never dispatched.
 __global__ void sf_pack_mark_kernel(int2 *nodes, const int64_t *seg_off, int64_t n_seg,
                                     int64_t total, int classes) {
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= n_seg) return;
+    auto seg_len = [&](int64_t t) { return ((t + 1 < n_seg) ? seg_off[t + 1] : total) - seg_off[t]; };
     int64_t start = seg_off[s];
-    int64_t end = (s + 1 < n_seg) ? seg_off[s + 1] : total;  // one past the sentinel
-    if (end - start == 1) nodes[start].x = 2 * classes;
-    else nodes[end - 2].x += classes;
+    if (seg_len(s) == 1) {
+        int run = 1;
+        while (s + run < n_seg && seg_len(s + run) == 1 && run < (1 << 30)) ++run;
+        nodes[start] = make_int2(2 * classes, run);
+    } else {
+        nodes[start + seg_len(s) - 2].x += classes;
+    }
 }
 
 }  // namespace

@@ -9,7 +9,8 @@ tile of filter kl with statically named registers.  The channel's last entry car
 index + KT*9: its variant applies the entry and falls straight into the channel
 transition (skip the sentinel slot, advance the patch pointer, reload the 6x6 input
 patch, stop after the chunk's last channel) -- no extra dispatch per channel.  An
-empty channel's sentinel slot carries 2*KT*9 (transition only).  Why PTX: a
+empty channel's sentinel slot carries 2*KT*9 and, in its value field, the length of the
+run of empty channels it starts: one dispatch skips the whole run.  Why PTX: a
 C++ switch becomes a 6-level compare tree and spills; this is one indirect branch per
 nonzero and no per-channel call overhead.
 
@@ -133,12 +134,20 @@ def block(KT: int) -> str:
     e(f"add.u32 {CUR}, {CUR}, 8;")
     e("bra.uni N_%=;")
     # empty channel: the prefetched entry already belongs to the next channel
+    # empty channels: the slot's value field holds the length of the run of empty
+    # channels starting here (>= 1); skip the whole run (clipped to the chunk) with one
+    # dispatch and one patch load for the next non-empty channel
     e("E_%=:")
-    prefetch()
-    e(f"sub.u32 {CNT}, {CNT}, 1;")
+    e("mov.b32 r_ix, f_v;")
+    e(f"min.u32 r_ix, r_ix, {CNT};")
+    e(f"sub.u32 {CNT}, {CNT}, r_ix;")
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
     e("@p_end bra.uni D_%=;")
-    e(f"add.u32 {PP}, {PP}, {CHS};")
+    e(f"mad.lo.u32 {PP}, r_ix, {CHS}, {PP};")
+    e("add.u32 r_ix, r_ix, -1;")
+    e(f"mad.lo.u32 {CUR}, r_ix, 8, {CUR};")
+    e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
+    e(f"add.u32 {CUR}, {CUR}, 8;")
     load_patch(e, P, PP, RB)
     e("bra.uni N_%=;")
     e("D_%=:")

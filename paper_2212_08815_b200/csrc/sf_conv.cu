@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
     // markers, so the dispatch call needs no enclosing branch.
     if (!live)
         for (int i = lane; i < STAGES * p.ent_cap; i += 32)
-            ent_s[((i / p.ent_cap) * NWARP + warp) * p.ent_cap + i % p.ent_cap] = make_int2(2 * KT * 9, 0);
+            ent_s[((i / p.ent_cap) * NWARP + warp) * p.ent_cap + i % p.ent_cap] =
+                make_int2(2 * KT * 9, 0x7fffffff);  // one run covering the whole chunk
     if (lane == 0)
         for (int ch = 0; ch < STAGES && ch < n_chunks; ++ch) {
             refill_entries(ch);

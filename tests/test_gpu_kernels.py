@@ -123,6 +123,10 @@ def test_sf_fast_config1_within_tolerance(dev):
         (4, 24, 12, 14, 14, 0.5, 4),
         (2, 9, 16, 27, 30, 0.8, 0),
         (1, 12, 8, 50, 41, 0.9, 8),
+        # runs of empty channels (one dispatch skips a run, clipped to the chunk)
+        (2, 48, 40, 20, 20, 0.99, 4),
+        (1, 37, 12, 16, 16, 1.0, 4),
+        (2, 70, 8, 12, 12, 0.97, 2),
     ],
 )
 def test_sf_fast_matches_oracle(dev, oracle, n, c, k, h, w, zf, ly):
