@@ -131,6 +131,46 @@ class VGGEngine:
         device.whc_to_halo(x_whc, n, self.in_c, self.hw, self.hw, self._in)
         return device.halo_to_whc(self.run(self._in), self.out_hw)
 
+    def forward_from_host(self, h_src: torch.Tensor, n: int, fill=None) -> torch.Tensor:
+        """Pinned host (W,H,C)-memory images -> device (W,H,C) outputs.
+
+        The H2D copy runs on a side stream in two halves; the first conv runs per half
+        as soon as its half has landed, so the second half's copy overlaps compute.
+        Later layers run on the whole batch.  ``fill(lo, hi)``, if given, writes images
+        lo..hi-1 into ``h_src`` just before their half is copied (host packing of the
+        second half then overlaps the first half's copy and conv).
+        """
+        bufs = self._buffers(n)
+        elems = self.in_c * self.hw * self.hw
+        if getattr(self, "_d_in_n", None) != n:
+            self._d_in = torch.empty(n * elems, dtype=torch.float32, device=self._in.device)
+            self._d_in_n = n
+            self._copy_stream = torch.cuda.Stream(device=self._in.device)
+        cur = torch.cuda.current_stream()
+        cp = self._copy_stream
+        cp.wait_stream(cur)  # the previous call's readers of _d_in are done
+        halves = [(0, n // 2), (n // 2, n)] if n >= 2 else [(0, n)]
+        events = []
+        first = self.steps[0]
+        for lo, hi in halves:
+            if fill is not None:
+                fill(lo, hi)
+            with torch.cuda.stream(cp):
+                self._d_in[lo * elems:hi * elems].copy_(h_src[lo * elems:hi * elems], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cp)
+            cur.wait_event(ev)
+            device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
+                               self._in[lo:hi])
+            device.sf_conv3x3(self._in[lo:hi], first.bank, first.bias, relu=True, pool=first.pool,
+                              out=bufs[0][lo:hi], w=self.hw, ly=first.ly)
+        cur_buf, w = bufs[0], self.hw // 2 if first.pool else self.hw
+        for st, out in zip(self.steps[1:], bufs[1:]):
+            device.sf_conv3x3(cur_buf, st.bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly)
+            cur_buf = out
+            w = w // 2 if st.pool else w
+        return device.halo_to_whc(cur_buf, self.out_hw)
+
     def forward_device(self, x: torch.Tensor) -> torch.Tensor:
         """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer)."""
         assert x.shape[1] == self.in_c and x.shape[2] == self.hw and x.shape[3] == self.hw

@@ -348,30 +348,6 @@ def pinned_batch(n: int, dims) -> list:
     return [DenseTensor3((c, h, w), arr[i]) for i in range(n)]
 
 
-def _pack_to_device(batch, h_in, elems):
-    """Host pack into pinned staging on a few threads, each chunk's H2D issued as soon
-    as it is packed (copies overlap packing); returns the device buffer."""
-    import torch
-    from concurrent.futures import ThreadPoolExecutor
-
-    n = len(batch)
-    np_in = h_in.numpy().reshape(-1)
-    d_in = torch.empty(n * elems, dtype=torch.float32, device="cuda")
-    chunks = min(n, 8)
-    bounds = [(n * j // chunks, n * (j + 1) // chunks) for j in range(chunks)]
-
-    def pack(rng):
-        lo, hi = rng
-        for i in range(lo, hi):
-            np_in[i * elems:(i + 1) * elems] = batch[i].data  # numpy releases the GIL here
-        return rng
-
-    with ThreadPoolExecutor(max_workers=chunks) as ex:
-        for lo, hi in ex.map(pack, bounds):
-            d_in[lo * elems:hi * elems].copy_(h_in[lo * elems:hi * elems], non_blocking=True)
-    return d_in
-
-
 def _forward_engine(prepared: PreparedNet, batch) -> list:
     import torch
 
@@ -382,15 +358,21 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
     elems = c * h * w
     h_in, h_out = _staging.get(n, elems, oc * ohw * ohw)
     src = _staging.pinned_source(batch, elems)
-    if src is not None:
-        d_in = src.to("cuda", non_blocking=True)
-    else:
-        d_in = _pack_to_device(batch, h_in, elems)
-    whc = eng.forward_whc(d_in, n)
+    fill = None
+    if src is None:  # pageable inputs: pack each half into pinned staging just before its copy
+        np_in = h_in.numpy().reshape(n, elems)
+
+        def fill(lo, hi):
+            for i in range(lo, hi):
+                np_in[i] = batch[i].data
+
+        src = h_in
+    whc = eng.forward_from_host(src, n, fill)
     h_out.copy_(whc.view(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    out = h_out.numpy().reshape(n, -1)
-    return [DenseTensor3((oc, ohw, ohw), out[i].copy()) for i in range(n)]
+    # one copy out of the staging buffer; the returned tensors view that private array
+    out = h_out.numpy().reshape(n, -1).copy()
+    return [DenseTensor3((oc, ohw, ohw), out[i]) for i in range(n)]
 
 
 def _run_step(step: _Step, x, variant: str, strat):

@@ -53,7 +53,13 @@ def pack():
         np_in[i] = t.data
 
 
+pinned = network.pinned_batch(n, (3, 224, 224))
+for i in range(n):
+    pinned[i].data[:] = batch[i].data
+d_w = torch.empty(n * 3 * 224 * 224, dtype=torch.float32, device="cuda")
 res = {
+    "forward_total_pinned": timed(lambda: network.forward(prepared, pinned)),
+    "forward_whc": timed(lambda: eng.forward_whc(d_w, n)),
     "forward_total": timed(lambda: network.forward(prepared, batch)),
     "host_pack": timed(pack),
     "h2d": timed(lambda: d_in.copy_(h_in, non_blocking=True)),
