@@ -342,7 +342,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl.vgg16_weights(seed=103, zero_frac=zf), hw, sample_images=8)
+        cpu = cpu_baseline(wl.vgg16_weights(seed=103, zero_frac=zf), hw, sample_images=64)
 
     if rank == 0:
         peaks = _peaks()
