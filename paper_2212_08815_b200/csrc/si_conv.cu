@@ -10,6 +10,7 @@
 // Results equal to zero are written as +0.0 (the reference stores no node and
 // densify yields +0.0), then + bias[k] when a bias is given (layers.py:425-428).
 #include <algorithm>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -112,6 +113,68 @@ __global__ void __launch_bounds__(128, 8)
     }
 }
 
+// Shallow-bank variant (C <= 128): the strip kernel's weight loads dominate it (L2-bound,
+// 16 B per node per lane).  Here a persistent CTA keeps its 32-filter block's whole
+// [c][kh][32] float4 bank in shared memory (1.5 KB per channel) and walks many strips, so
+// every weight comes from shared memory; per-output order and arithmetic are the strip
+// kernel's (bit-exact).
+template <int S>
+__global__ void __launch_bounds__(512)
+    si_strip_smem_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int n_img,
+                         int c_n, int h_i, int w_i, const float4 *__restrict__ wq, int k_n, int strips,
+                         const float *__restrict__ bias, float *__restrict__ y) {
+    extern __shared__ float4 ws[];  // [c_n * 3][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int k = blockIdx.y * 32 + lane;
+    const bool live = k < k_n;
+    for (int idx = threadIdx.x; idx < c_n * 3 * 32; idx += blockDim.x) {
+        const int row = idx >> 5, kk = blockIdx.y * 32 + (idx & 31);
+        ws[idx] = kk < k_n ? wq[(int64_t)row * k_n + kk] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    const int64_t jobs = (int64_t)n_img * h_i * strips;
+    for (int64_t job = (int64_t)blockIdx.x * nwarp + warp; job < jobs; job += (int64_t)gridDim.x * nwarp) {
+        const int img = (int)(job / ((int64_t)h_i * strips));
+        const int rem = (int)(job % ((int64_t)h_i * strips));
+        const int i = rem / strips, j0 = (rem % strips) * S;
+        const int64_t *so = seg_off + (int64_t)img * h_i * w_i;
+        float acc[S];
+#pragma unroll
+        for (int t = 0; t < S; ++t) acc[t] = 0.0f;
+#pragma unroll
+        for (int col = 0; col < S + 2; ++col) {
+            const int w_in = j0 - 1 + col;
+            if (w_in < 0 || w_in >= w_i) continue;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+                const int h_in = i - 1 + kk;
+                if (h_in < 0 || h_in >= h_i) continue;
+                int64_t q = so[(int64_t)w_in * h_i + h_in];
+                for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) {
+                    const float v = __int_as_float(nd.y);
+                    const float4 wv = ws[(nd.x * 3 + kk) * 32 + lane];
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) {
+                        const int jp = col - l;
+                        if (jp < 0 || jp >= S) continue;
+                        const float wl = l == 0 ? wv.x : (l == 1 ? wv.y : wv.z);
+                        acc[jp] = __fadd_rn(acc[jp], __fmul_rn(wl, v));
+                    }
+                }
+            }
+        }
+        if (!live) continue;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+            const int j = j0 + t;
+            if (j >= w_i) break;
+            float v = (acc[t] != 0.0f) ? acc[t] : 0.0f;
+            if (bias) v = __fadd_rn(v, bias[k]);
+            y[(((int64_t)img * k_n + k) * h_i + i) * w_i + j] = v;
+        }
+    }
+}
+
 __global__ void kcrs_to_ckq_kernel(const float *__restrict__ w, int k_n, int c_n,
                                    float4 *__restrict__ out) {
     int64_t total = (int64_t)c_n * 3 * k_n;
@@ -155,6 +218,31 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
     auto warps_for = [&](int s_) { return (int64_t)n * h * ceil_div(w, s_) * k_blocks; };
     const int S = warps_for(8) >= 148 * 24 ? 8 : (warps_for(4) >= 148 * 24 ? 4 : 2);
     const int strips = (int)ceil_div(w, S);
+    const size_t ws_bytes = (size_t)c * 3 * 32 * sizeof(float4);
+    // Shared-memory weights pay off when two 512-thread CTAs still fit per SM (C <= 66)
+    // or when the problem is too small to fill the GPU anyway (one image, e.g. config 2:
+    // 43 -> 23 us); for C = 128 at batch 32 the halved occupancy costs more than the
+    // L2 weight traffic it saves (measured, tools/prof_si.py).
+    const bool small = warps_for(S) < 148 * 24;
+    if (ws_bytes <= 200 * 1024 && (ws_bytes <= 100 * 1024 || small) && getenv("FSCNN_SI_NOSMEM") == nullptr) {
+        // shallow bank: weights in shared memory, persistent CTAs (1 or 2 per SM)
+        const int per_sm = ws_bytes <= 100 * 1024 ? 2 : 1;
+        const int64_t jobs = (int64_t)n * h * strips;
+        const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(ceil_div(148 * per_sm, k_blocks),
+                                                                    ceil_div(jobs, 16)));
+        dim3 g2((unsigned)ctas, (unsigned)k_blocks, 1);
+        auto launch = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
+            kern<<<g2, 512, ws_bytes, as_stream(stream)>>>(reinterpret_cast<const int2 *>(in_nodes), in_seg_off,
+                                                          n, c, h, w, reinterpret_cast<const float4 *>(wq), k,
+                                                          strips, bias, y);
+        };
+        if (S == 8) launch(si_strip_smem_kernel<8>);
+        else if (S == 4) launch(si_strip_smem_kernel<4>);
+        else launch(si_strip_smem_kernel<2>);
+        FSCNN_LAUNCH_CHECK("si_strip_smem_kernel");
+        return FSCNN_OK;
+    }
     dim3 grid((unsigned)ceil_div((int64_t)h * strips, 4), (unsigned)k_blocks, (unsigned)n);
     auto args = [&](auto kern) {
         kern<<<grid, 128, 0, as_stream(stream)>>>(reinterpret_cast<const int2 *>(in_nodes), in_seg_off, c,
