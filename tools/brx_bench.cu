@@ -1,6 +1,11 @@
-// Microbenchmark: cost of the fast kernel's jump-table dispatch loop on B200,
-// isolated from TMA/pipeline.  Each warp walks a smem entry list (random (kl,tap)
-// entries, a sentinel every `per` entries) through sf3x3_channel_looped.
+// Microbenchmark: the fast sparse-filter kernel's jump-table dispatch loop on B200,
+// isolated from TMA, the ring and the epilogue.  Each warp walks 64 channels of a smem
+// entry list through the generated sf3x3_chunk (8 chunks of 8 channels, patch reloaded
+// per channel) with either `per` random entries per channel or Binomial(36, DENSITY).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/brx_bench tools/brx_bench.cu
+//   tools/brx_bench PER [FIXED_TAP]          (FIXED_TAP >= 0: every entry the same case)
+//   tools/brx_bench 0 -1 0 DENSITY
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdlib>
@@ -74,18 +79,6 @@ int main(int argc, char **argv) {
         h[k].x = per > 0 ? 0 : 2 * FSCNN_SF3_KT * 9; h[k].y = 0; ++k;
     }
     for (int j = 0; j < 8; ++j) { h[k + j].x = FSCNN_SF3_KT * 9; h[k + j].y = 0; }
-    int mask_mode = argc > 3 ? atoi(argv[3]) : 0;
-    if (mask_mode) {
-        // per channel: m0, m1, then `per` values (distinct classes) -> 32-bit words
-        uint32_t *w = (uint32_t *)h; int q = 0; srand(1);
-        for (int c = 0; c < n_ch; ++c) {
-            unsigned long long m = 0; int got = 0;
-            while (got < per) { int j = rand() % 36; if (!(m >> j & 1)) { m |= 1ull << j; ++got; } }
-            w[q++] = (uint32_t)m; w[q++] = (uint32_t)(m >> 32);
-            for (int j = 0; j < per; ++j) { float v = 1e-3f; w[q++] = *(uint32_t *)&v; }
-        }
-        n_ent = (q + 1) / 2;  // in 8-byte units
-    }
     // chunk starts (entry index of every 8th channel)
     int hst[8];
     {
@@ -105,7 +98,7 @@ int main(int argc, char **argv) {
     cudaMalloc(&o, 148 * 512 * 4);
     cudaMalloc(&cyc, 148 * 8);
     int smem = (n_ent + 10) * 8 + 8 * 34 * 20 * 4;
-    auto kern = mask_mode ? bench<1> : bench<0>;
+    auto kern = bench<0>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int warps = 4; warps <= 16; warps *= 2) {
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -117,7 +110,7 @@ int main(int argc, char **argv) {
         long long c0; cudaMemcpy(&c0, cyc, 8, cudaMemcpyDeviceToHost);
         double disp = (per >= 0 ? (double)n_ch * per : (double)binom_total) * reps;
         double fl = 148.0 * warps * 32 * disp * 32;
-        printf("mask=%d per=%d fixed=%d warps/SM=%d: %.1f cycles/nonzero/warp, %.2f TFLOP/s (%s)\n", mask_mode, per, fixed, warps,
+        printf("per=%d fixed=%d warps/SM=%d: %.1f cycles/nonzero/warp, %.2f TFLOP/s (%s)\n", per, fixed, warps,
                c0 / disp, fl / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
