@@ -98,6 +98,8 @@ def test_dense_baseline_conv_bitwise(g):
 def test_dot_dense_sparse_bitwise(g):
     for i in range(6):
         sv = fs.SparseVector(int(g[f"dot{i}__length"]), nodes_from_i64(g[f"dot{i}__nodes"]))
+        again = fs.SparseVector.from_dense(sv.to_dense())  # the GPU encoder, 1-D
+        assert again.length == sv.length and again.nodes.tobytes() == sv.nodes.tobytes()
         got = fs.dot_dense_sparse(g[f"dot{i}__d"], sv)
         assert np.float32(got).tobytes() == np.float32(g[f"dot{i}__y"]).tobytes(), i
 
