@@ -168,6 +168,37 @@ def test_sf_fast_layouts_agree_bitwise(dev, n, h, w):
         assert outs[0] == outs[1] == outs[2]
 
 
+def test_sf_fast_fuzz_against_oracle(dev, oracle):
+    """Seeded random geometries through the fast kernel (every layout, ragged sizes,
+    densities from empty to dense, bias/ReLU/fused pool) against the oracle."""
+    rng = np.random.default_rng(20261020)
+    for case in range(24):
+        n = int(rng.integers(1, 4))
+        c = int(rng.integers(1, 70))
+        k = int(rng.integers(1, 80))
+        h = int(rng.integers(1, 40))
+        w = int(rng.integers(1, 40))
+        zf = float(rng.choice([0.0, 0.5, 0.9, 0.97, 1.0]))
+        ly = int(rng.choice([0, 2, 4, 8]))
+        relu = bool(rng.integers(0, 2))
+        pool = bool(rng.integers(0, 2)) and h % 2 == 0 and w % 2 == 0
+        x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+        wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+        wt[rng.random(wt.shape) < zf] = 0
+        bias = rng.standard_normal(k).astype(np.float32)
+        nodes, seg = oracle.encode_bank(wt)
+        ref = oracle.sf_conv(x, nodes, seg, k, 3, 3, 1, 1, bias)
+        if relu:
+            ref = oracle.relu(ref)
+        if pool:
+            ref = oracle.pool(ref, 2, 2, "max")
+        bank = dev.sf_pack(_t(wt))
+        y = dev.sf_conv3x3(dev.to_halo(_t(x)), bank, _t(bias), relu=relu, pool=pool, w=w, ly=ly)
+        got = dev.from_halo(y, w // 2 if pool else w).cpu().numpy()
+        assert got.shape == ref.shape, case
+        assert normwise_err(got, ref) <= FAST_TOL, (case, n, c, k, h, w, zf, ly, relu, pool)
+
+
 def test_sf_fast_is_deterministic_and_batch_invariant(dev):
     import torch
 
@@ -226,6 +257,26 @@ def test_si_strip_kernel_bitwise(dev, oracle):
         segs = [oracle.encode(x[b], "CHW") for b in range(n)]
         oref = oracle.si_conv([s[0] for s in segs], [s[2] for s in segs], (c, h, wd), wt, 1, 1)
         assert np.array_equal(got, oref)
+
+
+def test_si_strip_paths_agree_bitwise(dev, monkeypatch):
+    """Every SI strip variant (shared-memory or L2 weights, strip width 8/4/2 picked by
+    problem size) computes the same bits as the gather kernel."""
+    rng = np.random.default_rng(31)
+    for (n, c, k, h, wd) in ((1, 64, 40, 20, 23), (4, 16, 96, 30, 30), (1, 130, 32, 9, 9), (6, 48, 64, 28, 28)):
+        x = np.abs(rng.standard_normal((n, c, h, wd))).astype(np.float32)
+        x[rng.random(x.shape) < 0.85] = 0
+        wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+        enc = dev.encode_order(_t(x), "CHW")
+        ref = dev.si_conv(enc.nodes, enc.seg_off, n, c, h, wd, dev.kcrs_to_crsk(_t(wt)), k, 3, 3, 1, 1).cpu().numpy()
+        wq = dev.si_pack3x3(_t(wt))
+        for nosmem in (False, True):
+            if nosmem:
+                monkeypatch.setenv("FSCNN_SI_NOSMEM", "1")
+            else:
+                monkeypatch.delenv("FSCNN_SI_NOSMEM", raising=False)
+            got = dev.si_conv3x3(enc.nodes, enc.seg_off, n, c, h, wd, wq, k).cpu().numpy()
+            assert np.array_equal(got.view(np.int32), ref.view(np.int32)), (n, c, k, h, wd, nosmem)
 
 
 def test_si_conv_config2(dev):
