@@ -319,3 +319,158 @@ void oracle_relu(const float *inp, int64_t n, float *out) {
         out[i] = (v > 0.0f || isnan(v)) ? v : 0.0f;
     }
 }
+
+/* ---------------------------------------------------------------------------
+ * Node-format activations.  Restates apply_activation's SparseTensor3 branch
+ * (layers.py:485-491) over rebuild_tensor3 (sparse_core.py:460-473): walk every
+ * segment's data nodes in buffer order; kind 0 (ReLU) keeps a node iff value > 0
+ * (value unchanged), kind 1 (LeakyReLU) maps v -> (v > 0 ? v : slope * v) and keeps
+ * the node iff the new value != 0; every segment ends with a sentinel; offsets are
+ * the running sum of (kept + 1).  out == NULL: count only.  Returns the node total.
+ * ------------------------------------------------------------------------- */
+int64_t oracle_rebuild(const node_t *nodes, const int64_t *seg_off, int64_t n_seg, int kind,
+                       float slope, int64_t *new_off, node_t *out) {
+    int64_t pos = 0;
+    for (int64_t s = 0; s < n_seg; ++s) {
+        new_off[s] = pos;
+        for (int64_t p = seg_off[s]; nodes[p].index != -1; ++p) {
+            float v = nodes[p].value, nv = v;
+            int keep;
+            if (kind == 0) {
+                keep = v > 0.0f;
+            } else {
+                nv = v > 0.0f ? v : slope * v;
+                keep = nv != 0.0f;
+            }
+            if (keep) {
+                if (out) {
+                    out[pos].index = nodes[p].index;
+                    out[pos].value = nv;
+                }
+                ++pos;
+            }
+        }
+        if (out) {
+            out[pos].index = -1;
+            out[pos].value = 0.0f;
+        }
+        ++pos;
+    }
+    return pos;
+}
+
+/* Batch norm, inference (layers.py:507-509) on a (W, H, C) payload:
+ * ((x - mean[c]) / sqrt(var[c] + eps)) * scale[c] + shift[c], float32 throughout. */
+void oracle_batchnorm(const float *inp, int c_n, int64_t hw, const float *scale, const float *shift,
+                      const float *mean, const float *var, float eps, float *out) {
+    for (int64_t q = 0; q < hw; ++q)
+        for (int c = 0; c < c_n; ++c) {
+            float sd = sqrtf(var[c] + eps);
+            out[q * c_n + c] = ((inp[q * c_n + c] - mean[c]) / sd) * scale[c] + shift[c];
+        }
+}
+
+/* pad_tensor, dense (layers.py:518-520): (W, H, C) -> (W+2p, H+2p, C), zeros around. */
+void oracle_pad_dense(const float *inp, int c_n, int h, int w, int p, float *out) {
+    int hp = h + 2 * p, wp = w + 2 * p;
+    for (int x = 0; x < wp; ++x)
+        for (int y = 0; y < hp; ++y)
+            for (int c = 0; c < c_n; ++c) {
+                int xi = x - p, yi = y - p;
+                out[((int64_t)x * hp + y) * c_n + c] =
+                    (xi >= 0 && xi < w && yi >= 0 && yi < h) ? inp[((int64_t)xi * h + yi) * c_n + c] : 0.0f;
+            }
+}
+
+/* pad_tensor, CHW nodes (layers.py:521-535): channel fibers keep their nodes; segment
+ * (w*H + h) moves to ((w+p)*(H+2p) + h+p); new border segments are empty.
+ * out == NULL: offsets only.  Returns the node total. */
+int64_t oracle_pad_chw_nodes(const node_t *nodes, const int64_t *seg_off, int h, int w, int p,
+                             int64_t *new_off, node_t *out) {
+    int hp = h + 2 * p, wp = w + 2 * p;
+    int64_t pos = 0;
+    for (int x = 0; x < wp; ++x)
+        for (int y = 0; y < hp; ++y) {
+            int64_t s = (int64_t)x * hp + y;
+            new_off[s] = pos;
+            int xi = x - p, yi = y - p;
+            if (xi >= 0 && xi < w && yi >= 0 && yi < h) {
+                for (int64_t q = seg_off[(int64_t)xi * h + yi]; nodes[q].index != -1; ++q) {
+                    if (out) out[pos] = nodes[q];
+                    ++pos;
+                }
+            }
+            if (out) {
+                out[pos].index = -1;
+                out[pos].value = 0.0f;
+            }
+            ++pos;
+        }
+    return pos;
+}
+
+/* transpose_matrix (kernels.py:360-380 over _transpose_segments_kernel :195-223):
+ * re-bucket n_seg segments by node index into seg_len new segments -- counts, running
+ * offsets (count + 1), scatter in buffer order with new index = old segment id, then
+ * the sentinels.  Values move untouched.  Returns the node total. */
+int64_t oracle_transpose_segments(const node_t *nodes, int64_t total, int64_t seg_len,
+                                  int64_t *new_off, node_t *out, int64_t *cursor /* seg_len */) {
+    for (int64_t i = 0; i < seg_len; ++i) cursor[i] = 0;
+    for (int64_t p = 0; p < total; ++p)
+        if (nodes[p].index != -1) ++cursor[nodes[p].index];
+    int64_t pos = 0;
+    for (int64_t i = 0; i < seg_len; ++i) {
+        new_off[i] = pos;
+        int64_t cnt = cursor[i];
+        cursor[i] = pos;
+        pos += cnt + 1;
+    }
+    int32_t seg = 0;
+    for (int64_t p = 0; p < total; ++p) {
+        if (nodes[p].index == -1) {
+            ++seg;
+        } else {
+            int64_t at = cursor[nodes[p].index]++;
+            out[at].index = seg;
+            out[at].value = nodes[p].value;
+        }
+    }
+    for (int64_t i = 0; i < seg_len; ++i) {
+        out[cursor[i]].index = -1;
+        out[cursor[i]].value = 0.0f;
+    }
+    return pos;
+}
+
+/* transpose_tensor3 WHC -> CHW (kernels.py:383-411): node (c, h, w, v) of segment
+ * (c*H + h) at index w moves to segment (w*H + h) at index c; new segments list their
+ * nodes with c ascending (the reference's per-channel re-bucket + (w, h, c) gather).
+ * Returns the node total. */
+int64_t oracle_transpose_whc_to_chw(const node_t *nodes, const int64_t *seg_off, int c_n, int h,
+                                    int w, int64_t *new_off, node_t *out, int64_t *cursor /* w*h */) {
+    int64_t n_new = (int64_t)w * h;
+    for (int64_t s = 0; s < n_new; ++s) cursor[s] = 0;
+    for (int c = 0; c < c_n; ++c)
+        for (int y = 0; y < h; ++y)
+            for (int64_t q = seg_off[(int64_t)c * h + y]; nodes[q].index != -1; ++q)
+                ++cursor[(int64_t)nodes[q].index * h + y];
+    int64_t pos = 0;
+    for (int64_t s = 0; s < n_new; ++s) {
+        new_off[s] = pos;
+        int64_t cnt = cursor[s];
+        cursor[s] = pos;
+        pos += cnt + 1;
+    }
+    for (int c = 0; c < c_n; ++c)
+        for (int y = 0; y < h; ++y)
+            for (int64_t q = seg_off[(int64_t)c * h + y]; nodes[q].index != -1; ++q) {
+                int64_t at = cursor[(int64_t)nodes[q].index * h + y]++;
+                out[at].index = c;
+                out[at].value = nodes[q].value;
+            }
+    for (int64_t s = 0; s < n_new; ++s) {
+        out[cursor[s]].index = -1;
+        out[cursor[s]].value = 0.0f;
+    }
+    return pos;
+}

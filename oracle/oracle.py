@@ -68,6 +68,19 @@ def lib():
         L.oracle_relu.restype = None
         L.oracle_relu.argtypes = [vp, i64, vp]
         L.oracle_has_openmp.restype = i32
+        f32 = ctypes.c_float
+        L.oracle_rebuild.restype = i64
+        L.oracle_rebuild.argtypes = [vp, vp, i64, i32, f32, vp, vp]
+        L.oracle_batchnorm.restype = None
+        L.oracle_batchnorm.argtypes = [vp, i32, i64, vp, vp, vp, vp, f32, vp]
+        L.oracle_pad_dense.restype = None
+        L.oracle_pad_dense.argtypes = [vp, i32, i32, i32, i32, vp]
+        L.oracle_pad_chw_nodes.restype = i64
+        L.oracle_pad_chw_nodes.argtypes = [vp, vp, i32, i32, i32, vp, vp]
+        L.oracle_transpose_segments.restype = i64
+        L.oracle_transpose_segments.argtypes = [vp, i64, i64, vp, vp, vp]
+        L.oracle_transpose_whc_to_chw.restype = i64
+        L.oracle_transpose_whc_to_chw.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -243,3 +256,79 @@ def vgg_forward(x_nchw, banks, threads=0):
             x = relu(sf_conv(x, nodes, seg, k_n, 3, 3, 1, 1, bias, threads))
             li += 1
     return x
+
+
+# -- sparse-input pipeline and node restructuring ------------------
+
+
+def rebuild(nodes, seg_off, kind: str, slope: float = 0.0):
+    """Node-format ReLU / LeakyReLU (layers.py:485-491 over sparse_core.py:460-473).
+    Returns (nodes, seg_off) of the rebuilt tensor (same order and dims)."""
+    nodes = np.ascontiguousarray(nodes)
+    seg = np.ascontiguousarray(seg_off, dtype=np.int64)
+    k = 0 if kind == "relu" else 1
+    new_off = np.empty(seg.size, np.int64)
+    L = lib()
+    total = L.oracle_rebuild(_p(nodes), _p(seg), seg.size, k, float(np.float32(slope)), _p(new_off), None)
+    out = np.empty(total, NODE_DTYPE)
+    L.oracle_rebuild(_p(nodes), _p(seg), seg.size, k, float(np.float32(slope)), _p(new_off), _p(out))
+    return out, new_off
+
+
+def batchnorm(x_chw, scale, shift, mean, var, eps):
+    """apply_batchnorm (layers.py:507-509) on a (C, H, W) array."""
+    x = np.asarray(x_chw, np.float32)
+    c, h, w = x.shape
+    whc = np.ascontiguousarray(x.transpose(2, 1, 0))
+    out = np.empty_like(whc)
+    f = lambda a: np.ascontiguousarray(a, np.float32)
+    sc, sh, mu, va = f(scale), f(shift), f(mean), f(var)
+    lib().oracle_batchnorm(_p(whc), c, h * w, _p(sc), _p(sh), _p(mu), _p(va), float(np.float32(eps)), _p(out))
+    return np.ascontiguousarray(out.transpose(2, 1, 0))
+
+
+def pad_dense(x_chw, p: int):
+    """pad_tensor on a dense (C, H, W) array (layers.py:518-520)."""
+    x = np.asarray(x_chw, np.float32)
+    c, h, w = x.shape
+    whc = np.ascontiguousarray(x.transpose(2, 1, 0))
+    out = np.empty((w + 2 * p, h + 2 * p, c), np.float32)
+    lib().oracle_pad_dense(_p(whc), c, h, w, p, _p(out))
+    return np.ascontiguousarray(out.transpose(2, 1, 0))
+
+
+def pad_chw_nodes(nodes, seg_off, dims_chw, p: int):
+    """pad_tensor on CHW nodes (layers.py:521-535): (nodes, seg_off) of the padded tensor."""
+    c, h, w = dims_chw
+    nodes = np.ascontiguousarray(nodes)
+    seg = np.ascontiguousarray(seg_off, dtype=np.int64)
+    new_off = np.empty((w + 2 * p) * (h + 2 * p), np.int64)
+    L = lib()
+    total = L.oracle_pad_chw_nodes(_p(nodes), _p(seg), h, w, p, _p(new_off), None)
+    out = np.empty(total, NODE_DTYPE)
+    L.oracle_pad_chw_nodes(_p(nodes), _p(seg), h, w, p, _p(new_off), _p(out))
+    return out, new_off
+
+
+def transpose_segments(nodes, seg_len: int):
+    """transpose_matrix's re-bucketing (kernels.py:195-223, :360-380): (nodes, seg_off)."""
+    nodes = np.ascontiguousarray(nodes)
+    data = int((nodes["index"] != -1).sum())
+    out = np.empty(data + seg_len, NODE_DTYPE)
+    new_off = np.empty(seg_len, np.int64)
+    cursor = np.empty(seg_len, np.int64)
+    lib().oracle_transpose_segments(_p(nodes), len(nodes), seg_len, _p(new_off), _p(out), _p(cursor))
+    return out, new_off
+
+
+def transpose_whc_to_chw(nodes, seg_off, dims_chw):
+    """transpose_tensor3 (kernels.py:383-411): WHC nodes -> CHW (nodes, seg_off)."""
+    c, h, w = dims_chw
+    nodes = np.ascontiguousarray(nodes)
+    seg = np.ascontiguousarray(seg_off, dtype=np.int64)
+    data = int((nodes["index"] != -1).sum())
+    out = np.empty(data + w * h, NODE_DTYPE)
+    new_off = np.empty(w * h, np.int64)
+    cursor = np.empty(w * h, np.int64)
+    lib().oracle_transpose_whc_to_chw(_p(nodes), _p(seg), c, h, w, _p(new_off), _p(out), _p(cursor))
+    return out, new_off

@@ -153,3 +153,41 @@ def test_density_evolution_matches_reference(g):
     assert np.array_equal(np.array([r.output_density for r in recs]), g["evo__density"])
     with pytest.raises(ValueError, match="sparse_input"):
         nw.density_evolution(net.with_variant("dense_baseline"), [0.5], 1)
+
+
+def test_pipeline_ops_at_layer_size_vs_oracle(oracle):
+    """The node-format ops on VGG16-layer-sized tensors (64 x 56 x 56, ~50 % dense, with
+    explicit +0.0 / -0.0 / NaN nodes) against the oracle's restatements, byte for byte."""
+    rng = np.random.default_rng(4242)
+    x = rng.standard_normal((64, 56, 56)).astype(np.float32)
+    x[rng.random(x.shape) < 0.5] = 0
+    base = fs.sparsify_tensor3(fs.DenseTensor3.from_array(x), fs.AxisOrder3.CHW)
+    nodes = base.nodes.copy()
+    data = np.nonzero(nodes["index"] != -1)[0]
+    pick = rng.choice(data, size=60, replace=False)
+    nodes["value"][pick[:20]] = 0.0
+    nodes["value"][pick[20:40]] = -0.0
+    nodes["value"][pick[40:]] = np.nan
+    t = fs.SparseTensor3(base.order, base.dims, nodes, base.matrix_offsets, base.segment_offsets)
+    seg = np.asarray(t.segment_offsets, np.int64)
+    for kind, slope in (("relu", 0.0), ("leaky_relu", 0.1)):
+        got = fs.apply_activation(t, kind, slope)
+        want_nodes, want_seg = oracle.rebuild(nodes, seg, "relu" if kind == "relu" else "leaky", slope)
+        assert got.nodes.tobytes() == want_nodes.tobytes() and np.array_equal(got.segment_offsets, want_seg), kind
+    got = fs.pad_tensor(t, 2)
+    want_nodes, want_seg = oracle.pad_chw_nodes(nodes, seg, t.dims, 2)
+    assert got.nodes.tobytes() == want_nodes.tobytes() and np.array_equal(got.segment_offsets, want_seg)
+    dense = oracle.decode(nodes, seg, t.dims, "CHW")
+    pooled = fs.pool_sparse(t, (2, 2), "max")
+    want = oracle.pool(dense[None], 2, 2, "max")[0]
+    p_nodes, _, _, p_seg = oracle.encode_batch(want[None], "CHW")
+    assert pooled.nodes.tobytes() == p_nodes.tobytes() and np.array_equal(pooled.segment_offsets, p_seg[0])
+    sc, sh, mu = (rng.uniform(-1, 1, 64).astype(np.float32) for _ in range(3))
+    va = rng.uniform(0.5, 1.5, 64).astype(np.float32)
+    d = fs.DenseTensor3.from_array(dense)
+    got = fs.apply_batchnorm(d, fs.BatchNormParams(sc, sh, mu, va, 1e-5)).to_array()
+    assert got.tobytes() == oracle.batchnorm(dense, sc, sh, mu, va, 1e-5).tobytes()
+    whc = fs.sparsify_tensor3(d, fs.AxisOrder3.WHC)
+    got = fs.transpose_tensor3(whc)
+    want_nodes, want_seg = oracle.transpose_whc_to_chw(whc.nodes, np.asarray(whc.segment_offsets, np.int64), d.dims)
+    assert got.nodes.tobytes() == want_nodes.tobytes() and np.array_equal(got.segment_offsets, want_seg)

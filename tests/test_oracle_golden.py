@@ -129,3 +129,45 @@ def test_pool_and_relu_match_reference(oracle):
         assert np.array_equal(got, y, equal_nan=True), i
     got = oracle.relu(g["relu__x"])
     assert np.array_equal(got.view(np.int32), g["relu__y"].view(np.int32))
+
+
+def _g_sparse(g, key):
+    from conftest import nodes_from_i64
+
+    return (nodes_from_i64(g[f"{key}__nodes"]), g[f"{key}__segment_offsets"],
+            tuple(int(v) for v in g[f"{key}__dims"]), str(g[f"{key}__order"]))
+
+
+def test_oracle_pipeline_ops_pinned(oracle):
+    """The oracle's restatements of the sparse-input pipeline ops reproduce the
+    reference's own outputs byte for byte (tests/golden/pipeline.npz)."""
+    g = load_golden("pipeline.npz")
+    for i in range(int(g["n_node_cases"])):
+        key = f"n{i}"
+        nodes, seg, dims, order = _g_sparse(g, f"{key}_in")
+        for kind, slope, tag in (("relu", 0.0, "relu"), ("leaky", 0.1, "leaky")):
+            got_nodes, got_seg = oracle.rebuild(nodes, seg, kind, slope)
+            assert got_nodes.tobytes() == g[f"{key}_{tag}__nodes"].tobytes(), (key, tag)
+            assert np.array_equal(got_seg, g[f"{key}_{tag}__segment_offsets"]), (key, tag)
+        x = g[f"{key}_dense__x"]
+        bn = [g[f"{key}_bn__{f}"] for f in ("scale", "shift", "mean", "var")]
+        assert oracle.batchnorm(x, *bn, 1e-5).tobytes() == g[f"{key}_dense_bn__y"].tobytes(), key
+        p = int(g[f"{key}_pad__p"])
+        assert oracle.pad_dense(x, p).tobytes() == g[f"{key}_dense_pad__y"].tobytes(), key
+        if order == "CHW":
+            got_nodes, got_seg = oracle.pad_chw_nodes(nodes, seg, dims, p)
+            assert got_nodes.tobytes() == g[f"{key}_pad__nodes"].tobytes(), key
+            assert np.array_equal(got_seg, g[f"{key}_pad__segment_offsets"]), key
+    for i in range(6):
+        from conftest import nodes_from_i64
+
+        rows, cols = (int(v) for v in g[f"tm{i}_in__shape"])
+        seg_len = cols if str(g[f"tm{i}_in__order"]) == "WH" else rows
+        got_nodes, got_seg = oracle.transpose_segments(nodes_from_i64(g[f"tm{i}_in__nodes"]), seg_len)
+        assert got_nodes.tobytes() == g[f"tm{i}_out__nodes"].tobytes(), i
+        assert np.array_equal(got_seg, g[f"tm{i}_out__segment_offsets"]), i
+    for i in range(4):
+        nodes, seg, dims, _ = _g_sparse(g, f"tt{i}_in")
+        got_nodes, got_seg = oracle.transpose_whc_to_chw(nodes, seg, dims)
+        assert got_nodes.tobytes() == g[f"tt{i}_out__nodes"].tobytes(), i
+        assert np.array_equal(got_seg, g[f"tt{i}_out__segment_offsets"]), i
