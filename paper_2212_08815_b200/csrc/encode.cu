@@ -344,17 +344,34 @@ constexpr int kSfPackKt = 4;  // default filters per group (sf_conv.cu supports 
 // an empty segment's sentinel slot becomes (2*kt*9, run) where run >= 1 counts the
 // consecutive empty segments starting at it (the kernel skips a run with one dispatch,
 // clipping it to the channel chunk).  Other sentinel slots are never dispatched.
+// Row mask of a segment: bit r set iff some nonzero's tap row kh satisfies
+// kh <= r <= kh + 3 (the patch rows its FMAs read); a missing segment loads all rows.
+__device__ __forceinline__ int seg_row_mask(const int2 *nodes, const int64_t *seg_off, int64_t n_seg,
+                                            int64_t total, int64_t t) {
+    if (t >= n_seg) return 0x3f;
+    const int64_t a = seg_off[t], b = ((t + 1 < n_seg) ? seg_off[t + 1] : total) - 1;
+    int m = 0;
+    for (int64_t q = a; q < b; ++q) m |= 0xf << ((nodes[q].x % 9) / 3);
+    return m;
+}
+
 __global__ void sf_pack_mark_kernel(int2 *nodes, const int64_t *seg_off, int64_t n_seg,
                                     int64_t total, int classes) {
     int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= n_seg) return;
     auto seg_len = [&](int64_t t) { return ((t + 1 < n_seg) ? seg_off[t + 1] : total) - seg_off[t]; };
     int64_t start = seg_off[s];
+    // read everything this thread needs before anyone rewrites marks (the masks read
+    // plain entries; marks only change the index of a segment's last entry, whose
+    // kh is the same after % 9, and the sentinel slots, which masks never read)
     if (seg_len(s) == 1) {
         int run = 1;
-        while (s + run < n_seg && seg_len(s + run) == 1 && run < (1 << 30)) ++run;
-        nodes[start] = make_int2(2 * classes, run);
+        while (s + run < n_seg && seg_len(s + run) == 1 && run < (1 << 15)) ++run;
+        const int m = seg_row_mask(nodes, seg_off, n_seg, total, s + run);
+        nodes[start] = make_int2(2 * classes, run | (m << 16));
     } else {
+        const int m = seg_row_mask(nodes, seg_off, n_seg, total, s + 1);
+        nodes[start + seg_len(s) - 1].y = m;    // sentinel slot: the next channel's rows
         nodes[start + seg_len(s) - 2].x += classes;
     }
 }

@@ -10,7 +10,10 @@ index + KT*9: its variant applies the entry and falls straight into the channel
 transition (skip the sentinel slot, advance the patch pointer, reload the 6x6 input
 patch, stop after the chunk's last channel) -- no extra dispatch per channel.  An
 empty channel's sentinel slot carries 2*KT*9 and, in its value field, the length of the
-run of empty channels it starts: one dispatch skips the whole run.  Why PTX: a
+run of empty channels it starts (bits 0-15): one dispatch skips the whole run.  A
+transition loads only the patch rows the next channel's nonzeros touch: the row mask
+travels in the value field of the previous channel's sentinel slot (or bits 16-21 of
+an empty slot's value).  Why PTX: a
 C++ switch becomes a 6-level compare tree and spills; this is one indirect branch per
 nonzero and no per-channel call overhead.
 
@@ -40,11 +43,20 @@ TILE, PATCH = 4, 6
 
 
 
-def load_patch(e, P, PP, RB):
-    # RB: the row pitch operand (an immediate; PTX folds the constant expression)
+def load_patch(e, P, PP, RB, mask=None):
+    # RB: the row pitch operand (an immediate; PTX folds the constant expression).
+    # mask: register with one bit per patch row the channel's nonzeros touch (rows
+    # kh..kh+3 of each); rows outside it keep the previous channel's values, which no
+    # entry of this channel reads -- fewer shared-memory wavefronts on sparse channels.
     for r in range(PATCH):
-        e(f"ld.shared.v2.b64 {{{P(r, 0)}, {P(r, 1)}}}, [{PP}+{RB}*{r}];")
-        e(f"ld.shared.b64 {P(r, 2)}, [{PP}+{RB}*{r}+16];")
+        if mask is None:
+            e(f"ld.shared.v2.b64 {{{P(r, 0)}, {P(r, 1)}}}, [{PP}+{RB}*{r}];")
+            e(f"ld.shared.b64 {P(r, 2)}, [{PP}+{RB}*{r}+16];")
+        else:
+            e(f"and.b32 r_t, {mask}, {1 << r};")
+            e(f"setp.ne.u32 q_r, r_t, 0;")
+            e(f"@q_r ld.shared.v2.b64 {{{P(r, 0)}, {P(r, 1)}}}, [{PP}+{RB}*{r}];")
+            e(f"@q_r ld.shared.b64 {P(r, 2)}, [{PP}+{RB}*{r}+16];")
 
 
 def block(KT: int) -> str:
@@ -61,7 +73,8 @@ def block(KT: int) -> str:
     L = []
     e = L.append
     e("{")
-    e(".reg .pred p_end;")
+    e(".reg .pred p_end, q_r;")
+    e(".reg .b32 r_t, r_m;")
     e(".reg .b32 r_ix, r_i1, r_v1, r_a, r_b, r_c, r_d, r_e, r_f;")
     e(".reg .b32 r_cur, r_pp, r_cnt;")
     e(f"mov.b32 r_cur, {I_CUR};")
@@ -129,7 +142,8 @@ def block(KT: int) -> str:
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
     e("@p_end bra.uni D_%=;")
     e(f"add.u32 {PP}, {PP}, {CHS};")
-    load_patch(e, P, PP, RB)
+    e("mov.b32 r_m, r_v1;")  # the sentinel slot's value: the next channel's row mask
+    load_patch(e, P, PP, RB, "r_m")
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
     e(f"add.u32 {CUR}, {CUR}, 8;")
     e("bra.uni N_%=;")
@@ -139,6 +153,8 @@ def block(KT: int) -> str:
     # dispatch and one patch load for the next non-empty channel
     e("E_%=:")
     e("mov.b32 r_ix, f_v;")
+    e("shr.u32 r_m, r_ix, 16;")  # the next non-empty channel's row mask
+    e("and.b32 r_ix, r_ix, 65535;")
     e(f"min.u32 r_ix, r_ix, {CNT};")
     e(f"sub.u32 {CNT}, {CNT}, r_ix;")
     e(f"setp.eq.u32 p_end, {CNT}, 0;")
@@ -148,7 +164,7 @@ def block(KT: int) -> str:
     e(f"mad.lo.u32 {CUR}, r_ix, 8, {CUR};")
     e(f"ld.shared.v2.b32 {{r_i1, r_v1}}, [{CUR}];")
     e(f"add.u32 {CUR}, {CUR}, 8;")
-    load_patch(e, P, PP, RB)
+    load_patch(e, P, PP, RB, "r_m")
     e("bra.uni N_%=;")
     e("D_%=:")
     e("}")
