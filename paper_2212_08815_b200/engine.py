@@ -134,8 +134,8 @@ class VGGEngine:
     def forward_from_host(self, h_src: torch.Tensor, n: int, fill=None) -> torch.Tensor:
         """Pinned host (W,H,C)-memory images -> device (W,H,C) outputs.
 
-        The H2D copy runs on a side stream in two halves; the first conv runs per half
-        as soon as its half has landed, so the second half's copy overlaps compute.
+        The H2D copy runs on a side stream in up to four parts; the first conv runs per
+        part as soon as its part has landed, so later parts' copies overlap compute.
         Later layers run on the whole batch.  ``fill(lo, hi)``, if given, writes images
         lo..hi-1 into ``h_src`` just before their half is copied (host packing of the
         second half then overlaps the first half's copy and conv).
@@ -149,7 +149,8 @@ class VGGEngine:
         cur = torch.cuda.current_stream()
         cp = self._copy_stream
         cp.wait_stream(cur)  # the previous call's readers of _d_in are done
-        halves = [(0, n // 2), (n // 2, n)] if n >= 2 else [(0, n)]
+        parts = 4 if n >= 8 else (2 if n >= 2 else 1)
+        halves = [(n * j // parts, n * (j + 1) // parts) for j in range(parts)]
         events = []
         first = self.steps[0]
         for lo, hi in halves:

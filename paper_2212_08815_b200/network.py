@@ -356,7 +356,7 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
     c, h, w = prepared.net.input_dims
     oc, ohw = eng.out_c, eng.out_hw
     elems = c * h * w
-    h_in, h_out = _staging.get(n, elems, oc * ohw * ohw)
+    h_in, _ = _staging.get(n, elems, oc * ohw * ohw)
     src = _staging.pinned_source(batch, elems)
     fill = None
     if src is None:  # pageable inputs: pack each half into pinned staging just before its copy
@@ -368,10 +368,12 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
 
         src = h_in
     whc = eng.forward_from_host(src, n, fill)
-    h_out.copy_(whc.view(-1), non_blocking=True)
+    # outputs go straight into a fresh pinned buffer (torch's caching host allocator
+    # recycles it once the returned arrays are gone), no host-side copy
+    res = torch.empty(n * oc * ohw * ohw, dtype=torch.float32, pin_memory=True)
+    res.copy_(whc.view(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    # one copy out of the staging buffer; the returned tensors view that private array
-    out = h_out.numpy().reshape(n, -1).copy()
+    out = res.numpy().reshape(n, -1)
     return [DenseTensor3((oc, ohw, ohw), out[i]) for i in range(n)]
 
 
