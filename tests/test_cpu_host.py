@@ -40,6 +40,23 @@ def test_abi_rejects_bad_arguments_without_gpu():
         _lib.call("fscnn_pool2d", None, 1, 1, 4, 4, 0, 2, 1, None, None)
     with pytest.raises(_lib.FscnnError, match="exceeds"):
         _lib.call("fscnn_sf_conv_exact", None, 1, 1, 2, 2, None, None, 1, 5, 5, 1, 0, None, 0, None, None)
+    with pytest.raises(_lib.FscnnError, match="exceeds"):
+        _lib.call("fscnn_dense_conv_exact", None, 1, 1, 2, 2, None, 1, 5, 5, 1, 0, None, None, None)
+    with pytest.raises(_lib.FscnnError, match="activation kind"):
+        _lib.call("fscnn_activation", None, 0, 7, 0.0, None, None)
+    with pytest.raises(_lib.FscnnError, match="non-negative"):
+        _lib.call("fscnn_pad2d", None, 1, 1, 2, 2, -1, None, None)
+    with pytest.raises(_lib.FscnnError, match="null"):
+        _lib.call("fscnn_batchnorm", None, 1, 1, 2, 2, None, None, None, None, 1e-5, None, None)
+    with pytest.raises(_lib.FscnnError, match="negative extent"):
+        _lib.call("fscnn_encode_masked_offsets", None, None, -1, 1, 1, 1, 0, 0, 0, 0, None, None, None, 0, None)
+    with pytest.raises(_lib.FscnnError, match="negative extent"):
+        _lib.call("fscnn_remap_segments_offsets", None, -1, 0, None, 1, None, None, None, 0, None)
+    with pytest.raises(_lib.FscnnError, match="row pitch"):
+        _lib.call("fscnn_sf_conv3x3_ex", None, 1, 4, 8, 8, 6, None, None, 0, 1, 1, 4, None, 0, 0, None, 12,
+                  0, 4, None)
+    with pytest.raises(_lib.FscnnError, match="row pitch"):
+        _lib.call("fscnn_whc_to_nchw_ex", None, 1, 1, 4, 8, None, 8, 1, None)
 
 
 def test_no_cpu_fallback():
