@@ -154,6 +154,22 @@ __global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw,
     }
 }
 
+// Shallow images: one thread per output pixel (img, h, w) in NCHW order, so the c
+// plane writes coalesce; the (W,H,C) reads are C-float strided.
+__global__ void whc_to_nchw_small_kernel(const float *__restrict__ x, int64_t total, int c_n, int h, int w,
+                                         int ld, int col0, float *__restrict__ y) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int wi = (int)(t % w);
+        const int64_t r = t / w;
+        const int hi = (int)(r % h);
+        const int64_t img = r / h;
+        const float *src = x + ((img * w + wi) * (int64_t)h + hi) * c_n;
+        float *dst = y + (img * c_n * h + hi) * (int64_t)ld + col0 + wi;
+        for (int c = 0; c < c_n; ++c) dst[(int64_t)c * h * ld] = src[c];
+    }
+}
+
 __global__ void nchw_to_whc_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
                                    int ld, int col0, float *__restrict__ y) {
     __shared__ float tile[32][33];
@@ -270,6 +286,13 @@ int fscnn_whc_to_nchw_ex(const float *x_whc, int n, int c, int h, int w, float *
     FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
     FSCNN_REQUIRE(col0 >= 0 && ld >= w + col0, "row pitch too small");
     if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
+    if (c <= 8) {  // shallow images (the network input): a thread per pixel, no smem tile
+        const int64_t total = (int64_t)n * h * w;
+        whc_to_nchw_small_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(x_whc, total, c, h, w,
+                                                                                      ld, col0, y);
+        FSCNN_LAUNCH_CHECK("whc_to_nchw_small_kernel");
+        return FSCNN_OK;
+    }
     dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
     whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, ld, col0, y);
     FSCNN_LAUNCH_CHECK("whc_to_nchw_kernel");

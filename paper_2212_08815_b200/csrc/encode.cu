@@ -22,9 +22,23 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 // --- source walkers ----------------------------------------------------------
 
+// Thread t -> segment id for the thread-per-segment kernels.  Segments are numbered
+// (b, o, m) with m fastest; when the outer axis has the smaller memory stride (e.g. CHW
+// nodes of NCHW activations: segment (w, h), channels strided) neighbouring threads
+// take neighbouring o instead, so their fiber reads coalesce.
+__device__ __forceinline__ int64_t seg_of_thread(int64_t t, int64_t outer, int64_t mid, bool o_fast) {
+    if (!o_fast) return t;
+    const int64_t per = outer * mid;
+    const int64_t b = t / per, r = t - b * per;
+    const int64_t m = r / outer, o = r - m * outer;
+    return (b * outer + o) * mid + m;
+}
+
 struct StridedSrc {
     const float *p;
     int64_t outer, mid, inner, s_b, s_o, s_m, s_i;
+    bool o_fast;
+    __device__ __forceinline__ int64_t seg(int64_t t) const { return seg_of_thread(t, outer, mid, o_fast); }
     struct Fiber {
         const float *p;
     };
@@ -46,6 +60,8 @@ struct MaskedSrc {
     const float *p;
     const uint8_t *m;
     int64_t outer, mid, inner, s_b, s_o, s_m, s_i;
+    bool o_fast;
+    __device__ __forceinline__ int64_t seg(int64_t t) const { return seg_of_thread(t, outer, mid, o_fast); }
     struct Fiber {
         const float *p;
         const uint8_t *m;
@@ -66,6 +82,7 @@ struct SfPackSrc {
     const float *w;
     int64_t k, c, kt;
     int64_t inner;
+    __device__ __forceinline__ int64_t seg(int64_t t) const { return t; }
     struct Fiber {
         const float *p;
         int64_t kmax;
@@ -84,10 +101,12 @@ struct SfPackSrc {
 
 template <class Src>
 __global__ void count_thread_kernel(Src src, int64_t n_seg, int64_t *cnt) {
-    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_seg) return;
+    const int64_t s = src.seg(t);
     auto b = src.fiber(s);
     int64_t n = 0;
+#pragma unroll 8
     for (int64_t i = 0; i < src.inner; ++i) n += src.present(b, i);
     cnt[s] = n + 1;
 }
@@ -110,10 +129,12 @@ __global__ void count_warp_kernel(Src src, int64_t n_seg, int64_t *cnt) {
 template <class Src>
 __global__ void write_thread_kernel(Src src, int64_t n_seg, const int64_t *seg_off, int2 *nodes,
                                     int sentinel) {
-    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_seg) return;
+    const int64_t s = src.seg(t);
     auto b = src.fiber(s);
     int64_t p = seg_off[s];
+#pragma unroll 8
     for (int64_t i = 0; i < src.inner; ++i)
         if (src.present(b, i)) nodes[p++] = make_int2((int)i, __float_as_int(src.at(b, i)));
     nodes[p] = make_int2(sentinel, 0);
@@ -283,8 +304,9 @@ int encode_nodes_impl(const Src &src, int64_t n_seg, bool warp_mode, const int64
 __global__ void decode_kernel(const int2 *nodes, const int64_t *seg_off, int64_t n_seg,
                               int64_t outer, int64_t mid, int64_t inner, float *dst, uint8_t *mask,
                               int64_t d_b, int64_t d_o, int64_t d_m, int64_t d_i) {
-    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_seg) return;
+    const int64_t s = seg_of_thread(t, outer, mid, d_o < d_m);  // coalesced destination writes
     int64_t m = s % mid, bo = s / mid, o = bo % outer, b = bo / outer;
     const int64_t off = b * d_b + o * d_o + m * d_m;
     float *d = dst + off;
@@ -396,7 +418,7 @@ int fscnn_encode_offsets(const float *src, int64_t batch, int64_t outer, int64_t
     FSCNN_REQUIRE(total_nodes != nullptr, "total_nodes is NULL");
     int64_t n_seg = batch * outer * mid;
     FSCNN_REQUIRE(n_seg == 0 || (src != nullptr || inner == 0) && seg_off != nullptr, "null buffer");
-    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i};
+    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i, s_o < s_m};
     return encode_offsets_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, total_nodes,
                                workspace, workspace_bytes, as_stream(stream));
 }
@@ -409,7 +431,7 @@ int fscnn_encode_nodes(const float *src, int64_t batch, int64_t outer, int64_t m
     int64_t n_seg = batch * outer * mid;
     if (n_seg == 0) return FSCNN_OK;
     FSCNN_REQUIRE(seg_off != nullptr && nodes != nullptr, "null buffer");
-    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i};
+    StridedSrc w{src, outer, mid, inner, s_b, s_o, s_m, s_i, s_o < s_m};
     cudaStream_t st = as_stream(stream);
     int rc = encode_nodes_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, nodes, st);
     if (rc != FSCNN_OK) return rc;
@@ -458,7 +480,7 @@ int fscnn_encode_masked_offsets(const float *src, const uint8_t *mask, int64_t b
     FSCNN_REQUIRE(total_nodes != nullptr, "total_nodes is NULL");
     int64_t n_seg = batch * outer * mid;
     FSCNN_REQUIRE(n_seg == 0 || ((src && mask) || inner == 0) && seg_off != nullptr, "null buffer");
-    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i};
+    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i, s_o < s_m};
     return encode_offsets_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, total_nodes,
                                workspace, workspace_bytes, as_stream(stream));
 }
@@ -471,7 +493,7 @@ int fscnn_encode_masked_nodes(const float *src, const uint8_t *mask, int64_t bat
     int64_t n_seg = batch * outer * mid;
     if (n_seg == 0) return FSCNN_OK;
     FSCNN_REQUIRE(seg_off != nullptr && nodes != nullptr, "null buffer");
-    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i};
+    MaskedSrc w{src, mask, outer, mid, inner, s_b, s_o, s_m, s_i, s_o < s_m};
     cudaStream_t st = as_stream(stream);
     int rc = encode_nodes_impl(w, n_seg, use_warp_walker(inner, s_i), seg_off, nodes, st);
     if (rc != FSCNN_OK) return rc;
