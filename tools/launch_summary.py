@@ -30,9 +30,12 @@ def main():
         pk["launches"] += 1
         pk["time_s"] += launches[k].get("gpu__time_duration.sum", 0.0)
     sf = [launches[k] for k in ids if "sf3x3_kernel" in launches[k]["kernel"]]
-    # bench order: 3 warm-up steps, `steps` timed steps, then per-layer timing -> take the
-    # first timed step (launches 40..52 of the sf3x3 sequence when warmup=3)
-    step = sf[39:52] if len(sf) >= 52 else sf[:13]
+    # bench order: 3 warm-up steps, `steps` timed steps, then per-layer timing.  A step
+    # runs the 13 convs on two half-batch streams (26 launches): take the first timed
+    # step; per-launch figures below are per full-batch layer (the two halves summed),
+    # the unit bench.py's roofline uses.
+    per_step = 26
+    step = sf[3 * per_step:4 * per_step] if len(sf) >= 4 * per_step else sf[:per_step]
     tot_t = sum(s.get("gpu__time_duration.sum", 0) for s in step)
     tot_b = sum(s.get("dram__bytes_read.sum", 0) + s.get("dram__bytes_write.sum", 0) for s in step)
     out = {
@@ -47,7 +50,8 @@ def main():
         ],
         "step_sf3x3_time_s": tot_t,
         "step_sf3x3_dram_bytes": tot_b,
-        "sf3x3_dram_bytes_per_launch": tot_b / max(len(step), 1),
+        "sf3x3_dram_bytes_per_launch": tot_b / 13.0,
+        "note_per_launch": "per full-batch conv layer (step total / 13)",
     }
     json.dump(out, open(dst, "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "step_sf3x3"}, indent=1))

@@ -21,3 +21,23 @@ for parts in (1, 2, 4, 1, 2):
     b.record(); b.synchronize()
     same = torch.equal(y, ref)
     print(f"parts {parts}: {a.elapsed_time(b) / 10:.3f} ms  identical={same}", flush=True)
+
+# the same stack captured once in a CUDA graph (both streams), then replayed
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    eng.run(xh, 2)
+torch.cuda.current_stream().wait_stream(s)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    yg = eng.run(xh, 2)
+for _ in range(3):
+    g.replay()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(10):
+    g.replay()
+b.record(); b.synchronize()
+print(f"graph, parts 2: {a.elapsed_time(b) / 10:.3f} ms  identical={torch.equal(yg, ref)}", flush=True)
