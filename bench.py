@@ -317,9 +317,13 @@ def main():
         for i in range(n_local):
             batch[i].data[:] = DenseTensor3.from_array(x_np[i]).data
         pageable = [DenseTensor3.from_array(x_np[i]) for i in range(n_local)]
-        for _ in range(2):
-            network.forward(prepared, batch)
         e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+        # untimed warm-up of the public-API path (pinned-buffer caches, copy streams,
+        # both input kinds) so the timed passes see steady state
+        for _ in range(max(3, e2e_steps)):
+            network.forward(prepared, batch)
+        for _ in range(2):
+            network.forward(prepared, pageable)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
