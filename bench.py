@@ -362,7 +362,7 @@ def main():
                        "l2": "working set > L2 (activations 0.4 GB per layer at batch 32)"},
             "nnz_gflops": flops_img * n_local * world * args.steps / (elapsed_ms * 1e-3) / 1e9,
             "nnz_gflop_per_image": flops_img / 1e9,
-            "roofline": {"bound": "fp32", "kernel": "sf3x3_kernel (13 launches = whole step)",
+            "roofline": {"bound": "fp32", "kernel": "sf3x3_kernel: the 13 convs, each timed as one full-batch launch on its stream (the step runs them as two half-batch streams)",
                          "achieved": achieved_tf, "peak": peak_meas, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_meas,
                          "peak_source": "measured FFMA probe (fscnn_fp32_probe) on this GPU; "
