@@ -135,20 +135,25 @@ __global__ void maxpool2x2_kernel(const float *__restrict__ x, int64_t total, in
 // layout of the fast kernel: ld = halo pitch, col0 = 1).
 __global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
                                    int ld, int col0, float *__restrict__ y) {
+    // tile = 32 channels x 32 pixels, pixels enumerated in the destination's (h, w)
+    // order: the loads run along c (contiguous in (W,H,C)), the stores along w
     __shared__ float tile[32][33];
     int img = blockIdx.z;
     const float *src = x + (int64_t)img * c_n * hw;
     float *dst = y + (int64_t)img * c_n * h * ld + col0;
-    int c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;  // p = w*H + h in source order
+    int c0 = blockIdx.y * 32, q0 = blockIdx.x * 32;  // q = h*W + w
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        int p = p0 + j, c = c0 + threadIdx.x;
-        if (p < hw && c < c_n) tile[j][threadIdx.x] = src[(int64_t)p * c_n + c];
+        int q = q0 + j, c = c0 + threadIdx.x;
+        if (q < hw && c < c_n) {
+            int hi = q / w, wi = q - hi * w;
+            tile[j][threadIdx.x] = src[((int64_t)wi * h + hi) * c_n + c];
+        }
     }
     __syncthreads();
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        int c = c0 + j, p = p0 + threadIdx.x;
-        if (p < hw && c < c_n) {
-            int wi = p / h, hi = p % h;
+        int c = c0 + j, q = q0 + threadIdx.x;
+        if (q < hw && c < c_n) {
+            int hi = q / w, wi = q - hi * w;
             dst[((int64_t)c * h + hi) * ld + wi] = tile[threadIdx.x][j];
         }
     }
