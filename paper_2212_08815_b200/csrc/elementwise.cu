@@ -133,7 +133,83 @@ __global__ void maxpool2x2_kernel(const float *__restrict__ x, int64_t total, in
 // (W,H,C)-memory image -> NCHW, 32x32 smem transpose over (c, hw) per image.  The NCHW
 // side has row pitch ld and starts at column col0 (ld = w, col0 = 0: dense; the halo
 // layout of the fast kernel: ld = halo pitch, col0 = 1).
-__global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
+// (W,H,C) <-> NCHW: a CTA moves a tile of 32 channels x kTH rows x 32 columns.  Both
+// sides are read/written 128 B at a time, and the tile's kTH pixels of one column are
+// contiguous in (W,H,C) memory (so are its kTH rows of one channel in NCHW), which
+// keeps each CTA's DRAM traffic inside a few pages.  (A 32-pixel x 32-channel tile along
+// q = h*W + w spread its 32 (W,H,C) pixels H*C floats apart: 1.56 TB/s.)
+constexpr int kTH = 4, kTPitch = 32 * kTH + 1;
+
+__global__ void __launch_bounds__(256) whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int h, int w,
+                                                          int ld, int col0, float *__restrict__ y) {
+    __shared__ float tile[32 * kTPitch];
+    // channel tiles of one pixel tile are launched back to back (they share DRAM pages
+    // on the (W,H,C) side)
+    const int n_ct = (c_n + 31) / 32, n_wt = (w + 31) / 32;
+    const int c0 = (blockIdx.x % n_ct) * 32, pt = blockIdx.x / n_ct;
+    const int w0 = (pt % n_wt) * 32, h0 = (pt / n_wt) * kTH;
+    const int img = blockIdx.z, tx = threadIdx.x;
+    const float *src = x + (int64_t)img * c_n * h * w;
+    float *dst = y + (int64_t)img * c_n * h * ld + col0;
+#pragma unroll
+    for (int r = threadIdx.y; r < 32 * kTH; r += 8) {  // r = (w_l, h_l): loads along c
+        const int wl = r / kTH, hl = r % kTH;
+        if (w0 + wl < w && h0 + hl < h && c0 + tx < c_n)
+            tile[tx * kTPitch + hl * 32 + wl] = src[((int64_t)(w0 + wl) * h + h0 + hl) * c_n + c0 + tx];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = threadIdx.y; r < 32 * kTH; r += 8) {  // r = (c_l, h_l): stores along w
+        const int cl = r / kTH, hl = r % kTH;
+        if (w0 + tx < w && h0 + hl < h && c0 + cl < c_n)
+            dst[((int64_t)(c0 + cl) * h + h0 + hl) * ld + w0 + tx] = tile[cl * kTPitch + hl * 32 + tx];
+    }
+}
+
+// Shallow images: one thread per output pixel (img, h, w) in NCHW order, so the c
+// plane writes coalesce; the (W,H,C) reads are C-float strided.
+__global__ void whc_to_nchw_small_kernel(const float *__restrict__ x, int64_t total, int c_n, int h, int w,
+                                         int ld, int col0, float *__restrict__ y) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int wi = (int)(t % w);
+        const int64_t r = t / w;
+        const int hi = (int)(r % h);
+        const int64_t img = r / h;
+        const float *src = x + ((img * w + wi) * (int64_t)h + hi) * c_n;
+        float *dst = y + (img * c_n * h + hi) * (int64_t)ld + col0 + wi;
+        for (int c = 0; c < c_n; ++c) dst[(int64_t)c * h * ld] = src[c];
+    }
+}
+
+__global__ void __launch_bounds__(256) nchw_to_whc_kernel(const float *__restrict__ x, int c_n, int h, int w,
+                                                          int ld, int col0, float *__restrict__ y) {
+    __shared__ float tile[32 * kTPitch];
+    // channel tiles of one pixel tile are launched back to back (they share DRAM pages
+    // on the (W,H,C) side)
+    const int n_ct = (c_n + 31) / 32, n_wt = (w + 31) / 32;
+    const int c0 = (blockIdx.x % n_ct) * 32, pt = blockIdx.x / n_ct;
+    const int w0 = (pt % n_wt) * 32, h0 = (pt / n_wt) * kTH;
+    const int img = blockIdx.z, tx = threadIdx.x;
+    const float *src = x + (int64_t)img * c_n * h * ld + col0;
+    float *dst = y + (int64_t)img * c_n * h * w;
+#pragma unroll
+    for (int r = threadIdx.y; r < 32 * kTH; r += 8) {  // r = (c_l, h_l): loads along w
+        const int cl = r / kTH, hl = r % kTH;
+        if (w0 + tx < w && h0 + hl < h && c0 + cl < c_n)
+            tile[cl * kTPitch + hl * 32 + tx] = src[((int64_t)(c0 + cl) * h + h0 + hl) * ld + w0 + tx];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = threadIdx.y; r < 32 * kTH; r += 8) {  // r = (w_l, h_l): stores along c
+        const int wl = r / kTH, hl = r % kTH;
+        if (w0 + wl < w && h0 + hl < h && c0 + tx < c_n)
+            dst[((int64_t)(w0 + wl) * h + h0 + hl) * c_n + c0 + tx] = tile[tx * kTPitch + hl * 32 + wl];
+    }
+}
+
+// Narrow images (W < 32): 32 channels x 32 pixels taken along q = h*W + w.
+__global__ void whc_to_nchw_q_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
                                    int ld, int col0, float *__restrict__ y) {
     // tile = 32 channels x 32 pixels, pixels enumerated in the destination's (h, w)
     // order: the loads run along c (contiguous in (W,H,C)), the stores along w
@@ -159,23 +235,8 @@ __global__ void whc_to_nchw_kernel(const float *__restrict__ x, int c_n, int hw,
     }
 }
 
-// Shallow images: one thread per output pixel (img, h, w) in NCHW order, so the c
-// plane writes coalesce; the (W,H,C) reads are C-float strided.
-__global__ void whc_to_nchw_small_kernel(const float *__restrict__ x, int64_t total, int c_n, int h, int w,
-                                         int ld, int col0, float *__restrict__ y) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += stride) {
-        const int wi = (int)(t % w);
-        const int64_t r = t / w;
-        const int hi = (int)(r % h);
-        const int64_t img = r / h;
-        const float *src = x + ((img * w + wi) * (int64_t)h + hi) * c_n;
-        float *dst = y + (img * c_n * h + hi) * (int64_t)ld + col0 + wi;
-        for (int c = 0; c < c_n; ++c) dst[(int64_t)c * h * ld] = src[c];
-    }
-}
 
-__global__ void nchw_to_whc_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
+__global__ void nchw_to_whc_q_kernel(const float *__restrict__ x, int c_n, int hw, int h, int w,
                                    int ld, int col0, float *__restrict__ y) {
     __shared__ float tile[32][33];
     int img = blockIdx.z;
@@ -298,8 +359,14 @@ int fscnn_whc_to_nchw_ex(const float *x_whc, int n, int c, int h, int w, float *
         FSCNN_LAUNCH_CHECK("whc_to_nchw_small_kernel");
         return FSCNN_OK;
     }
-    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
-    whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, ld, col0, y);
+    if (w < 32) {
+        dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
+        whc_to_nchw_q_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h * w, h, w, ld, col0, y);
+        FSCNN_LAUNCH_CHECK("whc_to_nchw_q_kernel");
+        return FSCNN_OK;
+    }
+    dim3 grid((unsigned)(ceil_div(w, 32) * ceil_div(h, kTH) * ceil_div(c, 32)), 1, (unsigned)n);
+    whc_to_nchw_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x_whc, c, h, w, ld, col0, y);
     FSCNN_LAUNCH_CHECK("whc_to_nchw_kernel");
     return FSCNN_OK;
 }
@@ -314,8 +381,14 @@ int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int
     FSCNN_REQUIRE(n >= 0 && c >= 0 && h >= 0 && w >= 0, "negative extent");
     FSCNN_REQUIRE(col0 >= 0 && ld >= w + col0, "row pitch too small");
     if ((int64_t)n * c * h * w == 0) return FSCNN_OK;
-    dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
-    nchw_to_whc_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x, c, h * w, h, w, ld, col0, y_whc);
+    if (w < 32) {
+        dim3 grid((unsigned)ceil_div((int64_t)h * w, 32), (unsigned)ceil_div(c, 32), (unsigned)n);
+        nchw_to_whc_q_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x, c, h * w, h, w, ld, col0, y_whc);
+        FSCNN_LAUNCH_CHECK("nchw_to_whc_q_kernel");
+        return FSCNN_OK;
+    }
+    dim3 grid((unsigned)(ceil_div(w, 32) * ceil_div(h, kTH) * ceil_div(c, 32)), 1, (unsigned)n);
+    nchw_to_whc_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(x, c, h, w, ld, col0, y_whc);
     FSCNN_LAUNCH_CHECK("nchw_to_whc_kernel");
     return FSCNN_OK;
 }

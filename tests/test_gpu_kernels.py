@@ -68,11 +68,18 @@ def test_encoder_stack_and_warp_walker(dev, oracle):
     assert np.array_equal(enc.tensor_off.cpu().numpy(), ref_ten)
 
 
-def test_encoder_large_scan(dev, oracle):
-    """Many segments: exercises the multi-tile int64 scan."""
+@pytest.mark.parametrize("shape,zf", [((4, 16, 96, 100), 0.9), ((3, 45, 13, 37), 0.5), ((2, 70, 9, 16), 0.97)])
+def test_encoder_large_scan(dev, oracle, shape, zf):
+    """Many segments: exercises the multi-tile int64 scan and the tiled writer (ragged
+    channel chunks and position tiles, -0.0 / NaN / inf entries)."""
     rng = np.random.default_rng(8)
-    x = rng.standard_normal((4, 16, 96, 100)).astype(np.float32)
-    x[rng.random(x.shape) < 0.9] = 0
+    x = rng.standard_normal(shape).astype(np.float32)
+    x[rng.random(x.shape) < zf] = 0
+    flat = x.reshape(-1)
+    idx = rng.choice(flat.size, 12, replace=False)
+    flat[idx[:4]] = -0.0
+    flat[idx[4:8]] = np.nan
+    flat[idx[8:]] = np.inf
     enc = dev.encode_order(_t(x), "CHW")
     ref_nodes, _, _, ref_seg = oracle.encode_batch(x, "CHW")
     assert enc.n_nodes == len(ref_nodes)
@@ -306,8 +313,18 @@ def test_pool_relu_and_layouts(dev):
     r = dev.relu(_t(g["relu__x"])).cpu().numpy()
     assert np.array_equal(r.view(np.int32), g["relu__y"].view(np.int32))
     rng = np.random.default_rng(5)
-    x = rng.standard_normal((3, 37, 11, 13)).astype(np.float32)
-    whc = dev.nchw_to_whc(_t(x))
-    assert np.array_equal(whc.cpu().numpy(), x.transpose(0, 3, 2, 1))
-    back = dev.whc_to_nchw(whc, 3, 37, 11, 13)
-    assert np.array_equal(back.cpu().numpy(), x)
+    # narrow (q-tiled) and wide (column-tiled) kernels, ragged channel / row / column tiles
+    for shape in [(3, 37, 11, 13), (2, 45, 7, 70), (1, 64, 9, 32), (2, 8, 5, 33)]:
+        x = rng.standard_normal(shape).astype(np.float32)
+        n, c, h, w = shape
+        whc = dev.nchw_to_whc(_t(x))
+        assert np.array_equal(whc.cpu().numpy(), x.transpose(0, 3, 2, 1)), shape
+        back = dev.whc_to_nchw(whc, n, c, h, w)
+        assert np.array_equal(back.cpu().numpy(), x), shape
+        # halo-column buffers: logical column j at memory column j + 1, zero columns kept
+        hal = dev.halo_empty(n, c, h, w)
+        dev.whc_to_halo(whc.view(-1), n, c, h, w, hal)
+        hn = hal.cpu().numpy()
+        assert np.array_equal(hn[..., 1 : w + 1], x), shape
+        assert not hn[..., 0].any() and not hn[..., w + 1 :].any(), shape
+        assert np.array_equal(dev.halo_to_whc(hal, w).cpu().numpy(), x.transpose(0, 3, 2, 1)), shape
