@@ -198,6 +198,22 @@ int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w
 int fscnn_si_pack3x3(const float *w_kc33, int k, int c, float *wq, void *stream);
 int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
                      int w, const float *wq, int k, const float *bias, float *y, void *stream);
+/* 3x3 / stride 1 / pad 1 channel-major path (the same contraction as
+ * _conv_input_sparse_kernel, kernels.py:136-166, summed channel by channel: results
+ * within fp32 reassociation of the reference, north-star tolerance max|err| <=
+ * 1e-4 max|ref|; deterministic).  A CTA owns an 8x8 (or 4x8) output tile of one image
+ * and up to 256 filters; per 32-channel chunk it decodes the tile's input region into
+ * shared memory, then each lane (one filter) applies every nonzero input of a channel
+ * with that channel's 9 weights held in registers.  wf: [c][Kp/32][9][32] floats (tap =
+ * kh*3+kw, Kp = K rounded up to 32, zero-padded), built by fscnn_si_pack_fast from a
+ * dense [K][C][3][3] bank; fscnn_si_fast_bank_floats gives its size.  n_nodes: length of
+ * in_nodes (bounds the 32-node fiber reads).  Replaces the same call as
+ * fscnn_si_conv3x3 (layers.py:425-428 conv_forward_sparse_input). */
+int64_t fscnn_si_fast_bank_floats(int k, int c);
+int fscnn_si_pack_fast(const float *w_kc33, int k, int c, float *wf, void *stream);
+int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
+                          int c, int h, int w, const float *wf, int k, const float *bias, float *y,
+                          void *stream);
 
 /* ---------------------------------------------------------------------------
  * Dense layers between convolutions.

@@ -370,6 +370,38 @@ def si_conv3x3(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: in
     return out
 
 
+def si_pack_fast(w_kc33: torch.Tensor) -> torch.Tensor:
+    """Dense [K, C, 3, 3] bank -> the channel-major kernel's [C][Kp/(32 KT)][9][32][KT]
+    layout (KT = filters per lane: 2 for K >= 128, else 1; Kp = K rounded up to 32 KT)."""
+    w = w_kc33.contiguous()
+    k, c = int(w.shape[0]), int(w.shape[1])
+    n = int(_lib.load().fscnn_si_fast_bank_floats(k, c))
+    out = torch.empty(n, dtype=torch.float32, device=w.device)
+    call("fscnn_si_pack_fast", ptr(w), k, c, ptr(out), stream())
+    return out
+
+
+def si_fast_ctas(n: int, h: int, w: int, k: int) -> int:
+    """CTAs the channel-major SI kernel launches (mirrors si_fast_geom in si_fast.cu)."""
+    kt = 2 if k >= 128 else 1
+    groups = -(-k // (32 * kt))
+    nw = 8 if groups >= 8 else (4 if groups >= 4 else 2)
+    return n * -(-h // 4) * -(-w // 8) * -(-k // (32 * kt * nw))
+
+
+def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,
+                    wf: torch.Tensor, k: int, bias: torch.Tensor | None = None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+    """3x3/s1/p1 sparse-input conv, channel-major (fp32 reassociation of kernels.py:136-166,
+    held to the north-star 1e-4 normwise tolerance)."""
+    if out is None:
+        out = torch.empty((n, k, h, w), dtype=torch.float32, device=nodes.device)
+    n_nodes = int(nodes.numel() // 2)
+    call("fscnn_si_conv3x3_fast", ptr(nodes), ptr(seg_off), n_nodes, n, c, h, w, ptr(wf), k, ptr(bias), ptr(out),
+         stream())
+    return out
+
+
 # -- dense layers / layout ----------------------------------------------------------------
 
 

@@ -6,9 +6,10 @@ kernel.  Their results are therefore bit-identical, as the reference guarantees,
 independent of ``workers`` (accepted for API compatibility; layers.py:149-155).
 
 Kernel choice: 3x3 / stride 1 / pad 1 layers big enough to fill the GPU use the fast
-channel-major kernel (fp32 reassociation, held to 1e-4 normwise); smaller ones (one
-56x56 image, as config 1), any other geometry, or ``set_exact(True)`` / FSCNN_EXACT=1
-use the reference-order kernel, bit-exact with the reference.
+channel-major kernels (fp32 reassociation, held to 1e-4 normwise; sparse-filter and
+sparse-input alike); smaller ones (one 56x56 image, as config 1; config 2), any other
+geometry, or ``set_exact(True)`` / FSCNN_EXACT=1 use the reference-order kernels,
+bit-exact with the reference.
 """
 
 from __future__ import annotations
@@ -37,7 +38,8 @@ _EXACT = os.environ.get("FSCNN_EXACT", "0") == "1"
 
 
 def set_exact(flag: bool) -> None:
-    """Force the reference-order (bit-exact) sparse-filter kernel for every geometry."""
+    """Force the reference-order (bit-exact) sparse-filter and sparse-input kernels for
+    every geometry."""
     global _EXACT
     _EXACT = bool(flag)
 
@@ -186,7 +188,10 @@ def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, pad
     c, h, w = t_in.dims
     _, h_f, w_f = filters[0].dims
     kcrs = kernels.filters_to_device_kcrs(filters)
-    if (h_f, w_f, stride, padding) == (3, 3, 1, 1):
+    k = len(filters)
+    if (h_f, w_f, stride, padding) == (3, 3, 1, 1) and not _EXACT and device.si_fast_ctas(1, h, w, k) >= 148:
+        y = device.si_conv3x3_fast(nodes, seg, 1, c, h, w, device.si_pack_fast(kcrs), k)
+    elif (h_f, w_f, stride, padding) == (3, 3, 1, 1):
         y = device.si_conv3x3(nodes, seg, 1, c, h, w, device.si_pack3x3(kcrs), len(filters))
     else:
         y = device.si_conv(nodes, seg, 1, c, h, w, device.kcrs_to_crsk(kcrs), len(filters), h_f, w_f, stride, padding)

@@ -145,6 +145,31 @@ def test_sparse_input_layer_matches_reference_bitwise():
             assert np.array_equal(fs.densify_matrix(m), y[0]), i
 
 
+def test_sparse_input_layer_fast_path(oracle):
+    """A layer big enough for the channel-major SI kernel: within the north-star
+    tolerance of the oracle; set_exact(True) routes it to the bit-exact kernel."""
+    from paper_2212_08815_b200 import device
+
+    rng = np.random.default_rng(57)
+    c, k, h, w = 24, 128, 56, 112
+    assert device.si_fast_ctas(1, h, w, k) >= 148  # the fast path is taken
+    x = np.abs(rng.standard_normal((c, h, w))).astype(np.float32)
+    x[rng.random(x.shape) < 0.9] = 0
+    wt = rng.normal(0, 0.05, (k, c, 3, 3)).astype(np.float32)
+    bias = rng.standard_normal(k).astype(np.float32)
+    sp = fs.sparsify_tensor3(fs.DenseTensor3.from_array(x), fs.AxisOrder3.CHW)
+    filters = [fs.DenseTensor3.from_array(f) for f in wt]
+    nodes, _, seg = oracle.encode(x, "CHW")
+    ref = oracle.si_conv([nodes], [seg], (c, h, w), wt, 1, 1)[0] + bias[:, None, None]
+    fast = fs.conv_forward_sparse_input(sp, filters, 1, 1, bias).to_array()
+    assert normwise_err(fast, ref) <= TOL
+    fs.set_exact(True)
+    exact = fs.conv_forward_sparse_input(sp, filters, 1, 1, bias).to_array()
+    plane = oracle.si_conv([nodes], [seg], (c, h, w), wt, 1, 1)[0]
+    want = (plane + bias[:, None, None]).astype(np.float32)  # layers.py:425-428, fp32 add
+    assert np.array_equal(exact, want)
+
+
 def test_fusion_equals_unfused_exactly():
     rng = np.random.default_rng(56)
     for mode in ("max", "avg"):

@@ -286,6 +286,42 @@ def test_si_strip_paths_agree_bitwise(dev, monkeypatch):
             assert np.array_equal(got.view(np.int32), ref.view(np.int32)), (n, c, k, h, wd, nosmem)
 
 
+def test_si_fast_within_tolerance(dev, oracle):
+    """Channel-major SI kernel (one and two filters per lane) vs the bit-exact kernels /
+    oracle: north-star tolerance, ragged tiles, K and C off multiples of 32 / 64, empty
+    and fully dense inputs, several 32-channel chunks, bias."""
+    rng = np.random.default_rng(41)
+    cases = [(2, 37, 70, 13, 29, 0.8), (1, 5, 3, 1, 1, 0.5), (3, 64, 33, 28, 28, 0.9), (1, 130, 257, 9, 17, 0.95),
+             (2, 16, 64, 8, 8, 0.0), (1, 40, 32, 10, 12, 1.0), (4, 96, 128, 14, 14, 0.5),
+             (1, 70, 200, 11, 9, 0.0), (2, 100, 160, 7, 13, 0.9)]
+    for (n, c, k, h, wd, zf) in cases:
+        x = np.abs(rng.standard_normal((n, c, h, wd))).astype(np.float32)
+        x[rng.random(x.shape) < zf] = 0
+        wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+        bias = rng.standard_normal(k).astype(np.float32)
+        enc = dev.encode_order(_t(x), "CHW")
+        ref = dev.si_conv(enc.nodes, enc.seg_off, n, c, h, wd, dev.kcrs_to_crsk(_t(wt)), k, 3, 3, 1, 1,
+                          _t(bias)).cpu().numpy()
+        wf = dev.si_pack_fast(_t(wt))
+        got = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, wd, wf, k, _t(bias)).cpu().numpy()
+        assert normwise_err(got, ref) <= FAST_TOL, (n, c, k, h, wd, zf, normwise_err(got, ref))
+        # deterministic
+        again = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, wd, wf, k, _t(bias)).cpu().numpy()
+        assert np.array_equal(got.view(np.int32), again.view(np.int32))
+        if zf == 1.0:
+            assert np.array_equal(got, np.broadcast_to(bias[None, :, None, None], got.shape))
+    # against the oracle directly (no bias: dense plane, +0.0 where the sum is zero)
+    n, c, k, h, wd = 2, 48, 40, 12, 20
+    x = np.abs(rng.standard_normal((n, c, h, wd))).astype(np.float32)
+    x[rng.random(x.shape) < 0.9] = 0
+    wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+    enc = dev.encode_order(_t(x), "CHW")
+    got = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, wd, dev.si_pack_fast(_t(wt)), k).cpu().numpy()
+    segs = [oracle.encode(x[b], "CHW") for b in range(n)]
+    oref = oracle.si_conv([s[0] for s in segs], [s[2] for s in segs], (c, h, wd), wt, 1, 1)
+    assert normwise_err(got, oref) <= FAST_TOL
+
+
 def test_si_conv_config2(dev):
     import hashlib
 

@@ -1,0 +1,5 @@
+import sys,json
+for l in sys.stdin:
+    try: r=json.loads(l)
+    except Exception: print(l.strip()[:200]); continue
+    print(r["mode"], r["layer"], r["zero_frac"], round(r["ms"],3), round(r["tflops"],2), r.get("normwise_err_vs_exact",""))

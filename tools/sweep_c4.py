@@ -1,13 +1,15 @@
 """BASELINE config 4: per-layer sparsity sweep on the 13 VGG16 conv shapes at batch 32.
 
 Sparse-filter conv (fast kernel, fused ReLU, no pool) at filter sparsity
-{50,75,90,95,99}%, and sparse-input conv (encoder on the device-resident dense input
-+ the SI kernel) at input sparsity {50,75,90,95}%.  Each point: device time from
+{50,75,90,95,99}%, and sparse-input conv at input sparsity {50,75,90,95}% on the
+device-encoded input: the bit-exact strip kernel ("si") and the channel-major kernel
+("si_fast", with its normwise error against "si").  Each point: device time from
 CUDA events (median of reps), exact nnz-FLOPs, achieved TFLOP/s and fraction of the
 measured FP32 peak.  Writes JSON lines to stdout (one per point) and, with --out, a
 JSON file.
 
 usage: python tools/sweep_c4.py [--out profiles/r01_c4_sweep.json] [--layers 0,1,...] [--reps 5]
+       [--modes sf,si,si_fast]
 """
 import argparse
 import json
@@ -66,13 +68,15 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--peak", type=float, default=72.3, help="FP32 TFLOP/s denominator (measured probe)")
+    ap.add_argument("--modes", default="sf,si,si_fast")
     args = ap.parse_args()
     shapes = wl.vgg16_conv_shapes()
     layers = [int(v) for v in args.layers.split(",")] if args.layers else range(len(shapes))
     rows = []
     for li in layers:
         c, k, h, w = shapes[li]
-        for zf in (0.5, 0.75, 0.9, 0.95, 0.99):
+        modes = args.modes.split(",")
+        for zf in (0.5, 0.75, 0.9, 0.95, 0.99) if "sf" in modes else ():
             x, wt, b = wl.sweep_layer(li, "sf", zf, n=args.n)
             bank = device.sf_pack(torch.from_numpy(wt).cuda())
             xh = device.to_halo(torch.from_numpy(x).cuda())
@@ -86,21 +90,33 @@ def main():
             rows.append(r)
             print(json.dumps(r), flush=True)
             del xh, out, bank
-        for zf in (0.5, 0.75, 0.9, 0.95):
+        for zf in (0.5, 0.75, 0.9, 0.95) if ("si" in modes or "si_fast" in modes) else ():
             x, wt, b = wl.sweep_layer(li, "si", zf, n=args.n)
             xd = torch.from_numpy(x).cuda()
-            wq = device.si_pack3x3(torch.from_numpy(wt).cuda())
             enc = device.encode_order(xd, "CHW")
-            out = torch.empty((args.n, k, h, w), dtype=torch.float32, device="cuda")
-            ms = time_fn(lambda: device.si_conv3x3(enc.nodes, enc.seg_off, args.n, c, h, w, wq, k, out=out),
-                         args.reps)
             fl = si_flops(x, k)
-            r = {"mode": "si", "layer": li, "shape": [c, k, h, w], "zero_frac": zf, "ms": ms,
-                 "nnz_gflop": fl / 1e9, "tflops": fl / (ms * 1e-3) / 1e12}
-            r["frac_of_fp32_peak"] = r["tflops"] / args.peak
-            rows.append(r)
-            print(json.dumps(r), flush=True)
-            del xd, enc, out
+            ref = None
+            for mode in ("si", "si_fast"):
+                if mode not in modes:
+                    continue
+                out = torch.empty((args.n, k, h, w), dtype=torch.float32, device="cuda")
+                if mode == "si":
+                    wq = device.si_pack3x3(torch.from_numpy(wt).cuda())
+                    fn = lambda: device.si_conv3x3(enc.nodes, enc.seg_off, args.n, c, h, w, wq, k, out=out)
+                else:
+                    wf = device.si_pack_fast(torch.from_numpy(wt).cuda())
+                    fn = lambda: device.si_conv3x3_fast(enc.nodes, enc.seg_off, args.n, c, h, w, wf, k, out=out)
+                ms = time_fn(fn, args.reps)
+                r = {"mode": mode, "layer": li, "shape": [c, k, h, w], "zero_frac": zf, "ms": ms,
+                     "nnz_gflop": fl / 1e9, "tflops": fl / (ms * 1e-3) / 1e12}
+                r["frac_of_fp32_peak"] = r["tflops"] / args.peak
+                if mode == "si":
+                    ref = out
+                elif ref is not None:  # normwise error of the reassociated sum vs the exact kernel
+                    r["normwise_err_vs_exact"] = float((out - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+            del xd, enc, out, ref
         torch.cuda.empty_cache()
     if args.out:
         with open(args.out, "w") as fh:

@@ -22,6 +22,7 @@ def main():
     step_tf = c3["nnz_gflops"] / 1e3 if "nnz_gflops" in c3 else None
     sf = {z: c4_ranges(c4, "sf", z) for z in (0.5, 0.75, 0.9, 0.95, 0.99)}
     si = {z: c4_ranges(c4, "si", z) for z in (0.5, 0.9)}
+    sif = {z: c4_ranges(c4, "si_fast", z) for z in (0.5, 0.9)}
     text = f'''## 3. GPU results
 
 Measured on one B200 (148 SMs, SM clock {c3["clocks"]["sm_mhz"]:.0f} MHz under load, no throttle
@@ -38,7 +39,7 @@ reference path (`oracle/`, OpenMP) on the same box's {c3["cpu_baseline"]["cores"
 | C3: VGG16 @224², 90% zeros, batch 32 | images/s, inputs in HBM (`value`) | {c3["value"]:.0f} img/s ({c3["ms_per_step"]:.2f} ms/step = {c3["nnz_gflops"] / 1e3:.1f} nnz-TFLOP/s over the step); the kernel's launches average {c3["roofline"]["achieved"]:.2f} nnz-TFLOP/s = {100 * c3["roofline"]["frac"]:.1f} % of FP32 peak; DRAM {c3["roofline"]["traffic"] / 1e6:.0f} MB per layer vs {c3["roofline"]["algorithmic_bytes_per_launch"] / 1e6:.0f} MB algorithmic | `profiles/r01_bench_c3.json`, `profiles/r01_bench_launches_summary.json` |
 | C3 | images/s through `network.forward` with host buffers (`e2e`) | {c3["e2e"]["value"]:.0f} img/s (inputs in pinned memory); {c3["e2e"]["pageable"]["value"]:.0f} with pageable numpy inputs | same |
 | C3 | reference CPU path (oracle port, {c3["cpu_baseline"]["cores"]} threads, {c3["cpu_baseline"]["sample"].split(",")[0]}) | {c3["cpu_baseline"]["value"]:.2f} img/s → GPU e2e ×{c3["e2e"]["value"] / c3["cpu_baseline"]["value"]:.0f} | same, `profiles/r01_bench_reference.json` ({ref["value"]:.2f} img/s) |
-| C4: 13 layers × SF {{50,75,90,95,99}} % / SI {{50,75,90,95}} %, batch 32 | nnz-TFLOP/s per layer (L1–L12; L0 has 3 input channels) | SF 50 %: {sf[0.5]}, 75 %: {sf[0.75]}, 90 %: {sf[0.9]}, 95 %: {sf[0.95]}, 99 %: {sf[0.99]}; SI 50 %: {si[0.5]}, 90 %: {si[0.9]} | `profiles/r01_c4_sweep.json` |
+| C4: 13 layers × SF {{50,75,90,95,99}} % / SI {{50,75,90,95}} %, batch 32 | nnz-TFLOP/s per layer (L1–L12; L0 has 3 input channels) | SF 50 %: {sf[0.5]}, 75 %: {sf[0.75]}, 90 %: {sf[0.9]}, 95 %: {sf[0.95]}, 99 %: {sf[0.99]}; SI channel-major kernel 50 %: {sif[0.5]}, 90 %: {sif[0.9]} (the bit-exact strip kernel: {si[0.5]} / {si[0.9]}); normwise error of the channel-major kernel vs the exact one ≤ {max(r.get("normwise_err_vs_exact", 0) for r in c4):.1e} | `profiles/r01_c4_sweep.json` |
 | C5: VGG16, batch 256, 95 % zeros, 1 GPU | images/s | {c5["value"]:.0f} img/s ({c5["roofline"]["achieved"]:.2f} nnz-TFLOP/s per launch = {100 * c5["roofline"]["frac"]:.1f} %); e2e {c5["e2e"]["value"]:.0f} img/s; reference CPU path {ref5["value"]:.2f} img/s | `profiles/r01_bench_c5_1gpu.json`, `profiles/r01_bench_reference_c5.json` |
 | C5, 2/4/8 GPUs | images/s | not measurable here (gpurun gives one GPU); the batch-sharded driver's host logic is tested with gloo at world size 2 | — |
 
