@@ -78,8 +78,10 @@ def emit(ty, tx):
 def block2(ty, tx):
     """Two filters per lane: accumulator pair = (filter f0, filter f1) of one output,
     weight pair = (w_f0, w_f1) of one tap, value broadcast: every FMA is an FFMA2.
-    (Running the branch index one entry further ahead costs two register moves per
-    nonzero and measured 15 % slower.)"""
+    The next entry {pos, value} is loaded with one 64-bit shared load after the FMAs,
+    into the registers this case has finished with (no copies).  (Running the branch
+    index one entry further ahead costs two register moves per nonzero and measured
+    15 % slower.)"""
     ry_n, rx_n = ty + 2, tx + 2
     np_ = ry_n * rx_n
     na = ty * tx
@@ -89,28 +91,28 @@ def block2(ty, tx):
     L = []
     e = L.append
     e("{")
-    e(".reg .b32 r_cur, r_ix;")
+    e(".reg .b32 r_cur, r_ix, r_vb;")
     e(".reg .f32 f_v;")
     e(".reg .b64 d_vv;")
     e(f"mov.b32 r_cur, {I_CUR};")
     targets = ", ".join([f"P{p}_%=" for p in range(np_)] + ["D_%="])
     e(f"T_%=: .branchtargets {targets};")
-    e("ld.volatile.shared.b32 r_ix, [r_cur];")
-    e("ld.volatile.shared.f32 f_v, [r_cur+4];")
+    e("ld.volatile.shared.v2.b32 {r_ix, r_vb}, [r_cur];")
+    e("mov.b32 f_v, r_vb;")
     e("N_%=:")
     e("add.u32 r_cur, r_cur, 8;")
     e("brx.idx.uni r_ix, T_%=;")
     for p in range(np_):
         ry, rx = divmod(p, rx_n)
         e(f"P{p}_%=:")
-        e("ld.volatile.shared.b32 r_ix, [r_cur];")
         e("mov.b64 d_vv, {f_v, f_v};")
         for kh in range(3):
             for kw in range(3):
                 oy, ox = ry - kh, rx - kw
                 if 0 <= oy < ty and 0 <= ox < tx:
                     e(f"fma.rn.f32x2 {A(oy, ox)}, d_vv, {W(kh, kw)}, {A(oy, ox)};")
-        e("ld.volatile.shared.f32 f_v, [r_cur+4];")
+        e("ld.volatile.shared.v2.b32 {r_ix, r_vb}, [r_cur];")
+        e("mov.b32 f_v, r_vb;")
         e("bra.uni N_%=;")
     e("D_%=:")
     e("}")
