@@ -110,6 +110,12 @@ def main():
     us, gus = per_call_us(kern), graph_us(kern)
     res["c2_kernel"] = {"us_per_call": us, "us_per_call_graph": gus, "nnz_gflop": fl / 1e9,
                         "nnz_gflops": fl / (gus * 1e-6) / 1e9}
+    wf = device.si_pack_fast(torch.from_numpy(wt).cuda())
+    kern_f = lambda: device.si_conv3x3_fast(enc.nodes, enc.seg_off, 1, 128, 28, 28, wf, 128, out=y)
+    us, gus = per_call_us(kern_f), graph_us(kern_f)
+    res["c2_fast_kernel"] = {"us_per_call": us, "us_per_call_graph": gus, "nnz_gflop": fl / 1e9,
+                             "nnz_gflops": fl / (gus * 1e-6) / 1e9,
+                             "note": "channel-major kernel (28 CTAs here; the layer API keeps the exact one)"}
     layer = lambda: device.si_conv3x3(*(lambda e: (e.nodes, e.seg_off))(device.encode_order(xd, "CHW")), 1, 128,
                                       28, 28, wq, 128, out=y)
     res["c2_encode_plus_kernel"] = {"us_per_call": per_call_us(layer, calls=50),
