@@ -377,6 +377,135 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
     return [DenseTensor3((oc, ohw, ohw), out[i]) for i in range(n)]
 
 
+def _batched_inputs_ok(prepared: PreparedNet, batch) -> bool:
+    """The batched device path covers the dense and sparse_input variants for inputs the
+    per-image path would accept unchanged: CHW node tensors without explicit zero-valued
+    nodes (the batch travels as dense device planes, where a stored zero and an absent
+    node coincide) -- anything else takes the per-image path and its validation."""
+    variant = prepared.net.variant
+    if variant == VARIANT_SPARSE_FILTER or not prepared.steps:
+        return False
+    if variant == VARIANT_SPARSE_INPUT:
+        for t in batch:
+            if t.order is not AxisOrder3.CHW:
+                return False
+            nodes = np.asarray(t.nodes)
+            live = nodes["index"] >= 0
+            if np.any(nodes["value"][live] == 0):
+                return False
+    return True
+
+
+def _step_filters(step: _Step):
+    """Device copies of a conv step's filters (cached on the step): [K, C, R, S]."""
+    cache = getattr(step, "_dev_filters", None)
+    if cache is None:
+        from . import kernels
+
+        cache = kernels.filters_to_device_kcrs(step.params)
+        step._dev_filters = cache
+    return cache
+
+
+def _forward_batched(prepared: PreparedNet, batch) -> list:
+    """All images of the batch through the layer stack at once, activations resident in
+    HBM between steps (dense [N, C, H, W] planes; node-format steps are the same
+    decode -> op -> re-encode the per-image operators do, so each image's result is the
+    per-image result, bit for bit: every kernel is batch-position invariant and the
+    sparse-input kernel is chosen by the per-image rule)."""
+    import torch
+
+    from . import device
+    from .kernels import ConvGeometry
+
+    variant = prepared.net.variant
+    n = len(batch)
+    c, h, w = prepared.net.input_dims
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if variant == VARIANT_SPARSE_INPUT:
+        counts = [len(t.nodes) for t in batch]
+        base = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+        nodes = device.nodes_from_numpy(np.concatenate([np.asarray(t.nodes) for t in batch]))
+        seg = torch.from_numpy(np.concatenate([np.asarray(t.segment_offsets, np.int64) + b
+                                               for t, b in zip(batch, base)])).to(dev)
+        x = device.decode_order(nodes, seg, (n, c, h, w), "CHW")
+        sparse = True
+    else:
+        whc = torch.from_numpy(np.stack([np.asarray(t.data, np.float32) for t in batch])).to(dev)
+        x = device.whc_to_nchw(whc.view(-1), n, c, h, w)
+        sparse = False
+    for step in prepared.steps:
+        dims = tuple(int(v) for v in x.shape[1:])
+        if step.kind == "conv":
+            kcrs = _step_filters(step)
+            k, _, h_f, w_f = (int(v) for v in kcrs.shape)
+            geom = ConvGeometry(dims, (int(kcrs.shape[1]), h_f, w_f), step.stride, step.padding)
+            bias = torch.from_numpy(np.ascontiguousarray(step.bias, np.float32)).to(dev)
+            if sparse:
+                enc = device.encode_order(x, "CHW")
+                _, ci, hi, wi = (int(v) for v in x.shape)
+                if (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1) and not ly._EXACT and \
+                        device.si_fast_ctas(1, hi, wi, k) >= 148:
+                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack_fast(kcrs), k)
+                elif (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
+                    y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack3x3(kcrs), k)
+                else:
+                    y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, device.kcrs_to_crsk(kcrs), k, h_f,
+                                       w_f, step.stride, step.padding)
+                if step.fused_pool is not None:
+                    h_p, w_p = ly._pool_args(step.fused_pool, step.fused_pool_mode, geom.n_h, geom.n_w)
+                    y = device.pool2d(y, h_p, w_p, step.fused_pool_mode == ly.POOL_MAX)
+                if np.any(step.bias != 0):
+                    y = y + bias.view(1, -1, 1, 1)
+                    sparse = False
+            else:
+                y = device.dense_conv_exact(x, kcrs, step.stride, step.padding, bias)
+                if step.fused_pool is not None:
+                    h_p, w_p = ly._pool_args(step.fused_pool, step.fused_pool_mode, geom.n_h, geom.n_w)
+                    y = device.pool2d(y, h_p, w_p, step.fused_pool_mode == ly.POOL_MAX)
+            x = y
+        elif step.kind in ("maxpool", "avgpool"):
+            h_p, w_p = step.kernel
+            if h_p <= 0 or w_p <= 0:
+                raise ValueError(f"pool window must be positive, got {step.kernel}")
+            if dims[1] % h_p or dims[2] % w_p:
+                raise ValueError(f"input {dims[1]}x{dims[2]} not divisible by pool window {h_p}x{w_p}")
+            x = device.pool2d(x, h_p, w_p, step.kind == "maxpool")
+        elif step.kind in ("relu", "leaky_relu"):
+            if step.slope < 0:
+                raise ValueError("leaky slope must be non-negative")
+            if step.kind == "relu":
+                kind = device.ACT_RELU_NODES if sparse else device.ACT_RELU
+            else:
+                kind = device.ACT_LEAKY
+            x = device.activation(x, kind, step.slope)
+        elif step.kind == "batchnorm":
+            prm = step.params
+            prm.validate(dims[0])
+            x = device.batchnorm(x, prm.scale, prm.shift, prm.mean, prm.var, prm.epsilon)
+        elif step.kind == "pad":
+            if step.padding < 0:
+                raise ValueError("pad width must be non-negative")
+            if step.padding:
+                x = device.pad2d(x, step.padding)
+        else:
+            raise ValueError(f"unknown step kind {step.kind!r}")
+    oc, oh, ow = (int(v) for v in x.shape[1:])
+    if sparse:
+        enc = device.encode_order(x, "CHW")
+        nodes_h = device.nodes_to_numpy(enc.nodes, enc.n_nodes)
+        seg_h = enc.seg_off.cpu().numpy().reshape(n, ow * oh)
+        ten_h = np.append(enc.tensor_off.cpu().numpy(), enc.n_nodes)
+        outs = []
+        for i in range(n):
+            lo, hi_ = int(ten_h[i]), int(ten_h[i + 1])
+            so = seg_h[i] - lo
+            outs.append(SparseTensor3(AxisOrder3.CHW, (oc, oh, ow), nodes_h[lo:hi_].copy(), so[::oh].copy(), so))
+        return outs
+    whc = device.nchw_to_whc(x).cpu().numpy().reshape(n, -1)
+    return [DenseTensor3((oc, oh, ow), whc[i].copy()) for i in range(n)]
+
+
 def _run_step(step: _Step, x, variant: str, strat):
     """One step (network.py:410-448), every branch a GPU operator."""
     if step.kind == "conv":
@@ -417,6 +546,8 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
     t0 = time.perf_counter()
     if prepared.engine is not None and not record_density:
         outputs = _forward_engine(prepared, batch)
+    elif not record_density and _batched_inputs_ok(prepared, batch):
+        outputs = _forward_batched(prepared, batch)
     else:
         if not prepared.steps:
             raise NotImplementedError("per-layer execution needs a PreparedNet from prepare()")

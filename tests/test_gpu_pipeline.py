@@ -144,6 +144,49 @@ def test_network_variants_bitwise(g):
         fs.set_exact(False)
 
 
+def test_batched_forward_equals_per_image(g):
+    """forward() runs the dense and sparse_input variants as one batched device pass
+    (activations resident in HBM between steps); every image's output must be the
+    per-image path's (record_density=True keeps that path), bit for bit, and the golden
+    case's output the reference's.  Inputs with explicit zero-valued nodes take the
+    per-image path."""
+    import paper_2212_08815_b200.network as nwmod
+
+    for i in range(int(g["n_net_cases"])):
+        key = f"net{i}"
+        kind, variant, seed = str(g[f"{key}__kind"]), str(g[f"{key}__variant"]), int(g[f"{key}__seed"])
+        if variant == "sparse_filter":
+            continue
+        net = nw.build_benchmark_net(kind, 0.125, input_hw=32, variant=variant)
+        prepared = nw.prepare(net, nw.random_weights(net, seed))
+        xs = [fs.prune_random(nw.random_input(net.input_dims, seed), 0.4, seed)]
+        xs += [fs.prune_random(nw.random_input(net.input_dims, seed + j), 0.3 + 0.2 * j, seed + j) for j in (1, 2)]
+        inp = [fs.sparsify_tensor3(x, fs.AxisOrder3.CHW) if variant == "sparse_input" else x for x in xs]
+        assert nwmod._batched_inputs_ok(prepared, inp)
+        batched = nw.forward(prepared, inp).outputs
+        single = nw.forward(prepared, inp, record_density=True).outputs
+        for a, b in zip(batched, single):
+            assert type(a) is type(b), key
+            if isinstance(a, fs.SparseTensor3):
+                assert a.nodes.tobytes() == b.nodes.tobytes(), key
+                assert np.array_equal(a.segment_offsets, b.segment_offsets), key
+                assert np.array_equal(a.matrix_offsets, b.matrix_offsets), key
+            else:
+                assert np.array_equal(_bits(a.to_array()), _bits(b.to_array())), key
+        if isinstance(batched[0], fs.SparseTensor3):
+            _same_sparse(batched[0], g, f"{key}_out")
+        else:
+            assert np.array_equal(_bits(batched[0].to_array()), _bits(g[f"{key}_out__y"])), key
+        if variant == "sparse_input":
+            t = inp[0]
+            nodes = t.nodes.copy()
+            live = np.flatnonzero(nodes["index"] >= 0)
+            nodes["value"][live[0]] = 0.0  # an explicit zero node
+            z = fs.SparseTensor3(t.order, t.dims, nodes, t.matrix_offsets, t.segment_offsets)
+            assert not nwmod._batched_inputs_ok(prepared, [z])
+            nw.forward(prepared, [z])  # per-image path
+
+
 def test_density_evolution_matches_reference(g):
     net = nw.build_benchmark_net("vgg16_desk", 0.125, input_hw=32, variant="sparse_input")
     recs = nw.density_evolution(net, [0.1, 0.5, 1.0], 2020)
