@@ -377,6 +377,9 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
     return [DenseTensor3((oc, ohw, ohw), out[i]) for i in range(n)]
 
 
+_BATCHED = True  # tests switch it off to compare against the per-image layer path
+
+
 def _batched_inputs_ok(prepared: PreparedNet, batch) -> bool:
     """The batched device path covers the dense and sparse_input variants for inputs the
     per-image path would accept unchanged: CHW node tensors without explicit zero-valued
@@ -407,12 +410,14 @@ def _step_filters(step: _Step):
     return cache
 
 
-def _forward_batched(prepared: PreparedNet, batch) -> list:
+def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
     """All images of the batch through the layer stack at once, activations resident in
     HBM between steps (dense [N, C, H, W] planes; node-format steps are the same
     decode -> op -> re-encode the per-image operators do, so each image's result is the
     per-image result, bit for bit: every kernel is batch-position invariant and the
-    sparse-input kernel is chosen by the per-image rule)."""
+    sparse-input kernel is chosen by the per-image rule).  With ``densities`` (one list
+    per layer) each step's per-image density is appended, as density() of the per-image
+    output would give it (stored nodes = nonzeros of the plane)."""
     import torch
 
     from . import device
@@ -434,6 +439,7 @@ def _forward_batched(prepared: PreparedNet, batch) -> list:
         whc = torch.from_numpy(np.stack([np.asarray(t.data, np.float32) for t in batch])).to(dev)
         x = device.whc_to_nchw(whc.view(-1), n, c, h, w)
         sparse = False
+    counts = []  # (step, per-image nonzero counts on the device)
     for step in prepared.steps:
         dims = tuple(int(v) for v in x.shape[1:])
         if step.kind == "conv":
@@ -490,6 +496,14 @@ def _forward_batched(prepared: PreparedNet, batch) -> list:
                 x = device.pad2d(x, step.padding)
         else:
             raise ValueError(f"unknown step kind {step.kind!r}")
+        if densities is not None:
+            counts.append((step, torch.count_nonzero(x.reshape(n, -1), dim=1), x[0].numel()))
+    for step, cnt, size in counts:
+        for v in cnt.cpu().tolist():
+            d = float(v) / float(size)
+            densities[step.layer_index].append(d)
+            if step.fused_layer_index >= 0:
+                densities[step.fused_layer_index].append(d)
     oc, oh, ow = (int(v) for v in x.shape[1:])
     if sparse:
         enc = device.encode_order(x, "CHW")
@@ -546,8 +560,8 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
     t0 = time.perf_counter()
     if prepared.engine is not None and not record_density:
         outputs = _forward_engine(prepared, batch)
-    elif not record_density and _batched_inputs_ok(prepared, batch):
-        outputs = _forward_batched(prepared, batch)
+    elif _BATCHED and _batched_inputs_ok(prepared, batch):
+        outputs = _forward_batched(prepared, batch, densities)
     else:
         if not prepared.steps:
             raise NotImplementedError("per-layer execution needs a PreparedNet from prepare()")

@@ -144,13 +144,20 @@ def test_network_variants_bitwise(g):
         fs.set_exact(False)
 
 
-def test_batched_forward_equals_per_image(g):
+def test_batched_forward_equals_per_image(g, monkeypatch):
     """forward() runs the dense and sparse_input variants as one batched device pass
-    (activations resident in HBM between steps); every image's output must be the
-    per-image path's (record_density=True keeps that path), bit for bit, and the golden
+    (activations resident in HBM between steps); every image's output and recorded
+    layer densities must be the per-image layer path's, bit for bit, and the golden
     case's output the reference's.  Inputs with explicit zero-valued nodes take the
     per-image path."""
     import paper_2212_08815_b200.network as nwmod
+
+    def per_image(prepared, inp):
+        monkeypatch.setattr(nwmod, "_BATCHED", False)
+        try:
+            return nw.forward(prepared, inp, record_density=True)
+        finally:
+            monkeypatch.setattr(nwmod, "_BATCHED", True)
 
     for i in range(int(g["n_net_cases"])):
         key = f"net{i}"
@@ -163,8 +170,11 @@ def test_batched_forward_equals_per_image(g):
         xs += [fs.prune_random(nw.random_input(net.input_dims, seed + j), 0.3 + 0.2 * j, seed + j) for j in (1, 2)]
         inp = [fs.sparsify_tensor3(x, fs.AxisOrder3.CHW) if variant == "sparse_input" else x for x in xs]
         assert nwmod._batched_inputs_ok(prepared, inp)
-        batched = nw.forward(prepared, inp).outputs
-        single = nw.forward(prepared, inp, record_density=True).outputs
+        res_b = nw.forward(prepared, inp, record_density=True)
+        res_s = per_image(prepared, inp)
+        assert res_b.report.layer_densities == res_s.report.layer_densities, key
+        batched, single = res_b.outputs, res_s.outputs
+        assert all(type(a) is type(b) for a, b in zip(nw.forward(prepared, inp).outputs, batched))
         for a, b in zip(batched, single):
             assert type(a) is type(b), key
             if isinstance(a, fs.SparseTensor3):

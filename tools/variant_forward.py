@@ -1,6 +1,6 @@
 """Time network.forward for the dense_baseline and sparse_input variants: the batched
 device path (one launch per layer for the whole batch, activations in HBM) against the
-per-image path (record_density=True keeps it), and check they agree bit for bit.
+per-image layer path (network._BATCHED = False), and check they agree bit for bit.
 
 usage: python tools/variant_forward.py [--kind vgg16_desk] [--scale 1.0] [--hw 224] [--batch 8]
 """
@@ -36,9 +36,11 @@ def main():
         t0 = time.perf_counter()
         a = nw.forward(prepared, inp).outputs
         t_b = time.perf_counter() - t0
+        nw._BATCHED = False
         t0 = time.perf_counter()
-        b = nw.forward(prepared, inp, record_density=True).outputs
+        b = nw.forward(prepared, inp).outputs
         t_s = time.perf_counter() - t0
+        nw._BATCHED = True
         same = all((x.nodes.tobytes() == y.nodes.tobytes()) if isinstance(x, fs.SparseTensor3)
                    else np.array_equal(np.asarray(x.data).view(np.int32), np.asarray(y.data).view(np.int32))
                    for x, y in zip(a, b))
