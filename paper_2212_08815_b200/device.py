@@ -389,6 +389,15 @@ def si_fast_ctas(n: int, h: int, w: int, k: int) -> int:
     return n * -(-h // 4) * -(-w // 8) * -(-k // (32 * kt * nw))
 
 
+def si_use_fast(h: int, w: int, k: int) -> bool:
+    """The layer API's choice for a 3x3/s1/p1 sparse-input conv of one h x w image with k
+    filters: the channel-major kernel when one image already fills the GPU and the
+    filter count fills its 32-filter lane groups (K >= 64; below that most lanes of a
+    group would carry padding filters), else the bit-exact strip kernel.  Depends on the
+    image shape only, never on the batch, so batched and per-image runs agree bitwise."""
+    return k >= 64 and si_fast_ctas(1, h, w, k) >= 148
+
+
 def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,
                     wf: torch.Tensor, k: int, bias: torch.Tensor | None = None,
                     out: torch.Tensor | None = None) -> torch.Tensor:

@@ -189,7 +189,7 @@ def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, pad
     _, h_f, w_f = filters[0].dims
     kcrs = kernels.filters_to_device_kcrs(filters)
     k = len(filters)
-    if (h_f, w_f, stride, padding) == (3, 3, 1, 1) and not _EXACT and device.si_fast_ctas(1, h, w, k) >= 148:
+    if (h_f, w_f, stride, padding) == (3, 3, 1, 1) and not _EXACT and device.si_use_fast(h, w, k):
         y = device.si_conv3x3_fast(nodes, seg, 1, c, h, w, device.si_pack_fast(kcrs), k)
     elif (h_f, w_f, stride, padding) == (3, 3, 1, 1):
         y = device.si_conv3x3(nodes, seg, 1, c, h, w, device.si_pack3x3(kcrs), len(filters))

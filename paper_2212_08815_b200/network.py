@@ -381,12 +381,12 @@ _BATCHED = True  # tests switch it off to compare against the per-image layer pa
 
 
 def _batched_inputs_ok(prepared: PreparedNet, batch) -> bool:
-    """The batched device path covers the dense and sparse_input variants for inputs the
-    per-image path would accept unchanged: CHW node tensors without explicit zero-valued
-    nodes (the batch travels as dense device planes, where a stored zero and an absent
-    node coincide) -- anything else takes the per-image path and its validation."""
+    """The batched device path covers all three variants for inputs the per-image path
+    would accept unchanged (sparse_input: CHW node tensors without explicit zero-valued
+    nodes -- the batch travels as dense device planes, where a stored zero and an absent
+    node coincide); anything else takes the per-image path and its validation."""
     variant = prepared.net.variant
-    if variant == VARIANT_SPARSE_FILTER or not prepared.steps:
+    if not prepared.steps:
         return False
     if variant == VARIANT_SPARSE_INPUT:
         for t in batch:
@@ -443,15 +443,19 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
     for step in prepared.steps:
         dims = tuple(int(v) for v in x.shape[1:])
         if step.kind == "conv":
-            kcrs = _step_filters(step)
-            k, _, h_f, w_f = (int(v) for v in kcrs.shape)
-            geom = ConvGeometry(dims, (int(kcrs.shape[1]), h_f, w_f), step.stride, step.padding)
+            if variant == VARIANT_SPARSE_FILTER:
+                kcrs = None
+                k, c_f, h_f, w_f = (int(v) for v in step.params.dims)
+            else:
+                kcrs = _step_filters(step)
+                k, c_f, h_f, w_f = (int(v) for v in kcrs.shape)
+            geom = ConvGeometry(dims, (c_f, h_f, w_f), step.stride, step.padding)
             bias = torch.from_numpy(np.ascontiguousarray(step.bias, np.float32)).to(dev)
             if sparse:
                 enc = device.encode_order(x, "CHW")
                 _, ci, hi, wi = (int(v) for v in x.shape)
                 if (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1) and not ly._EXACT and \
-                        device.si_fast_ctas(1, hi, wi, k) >= 148:
+                        device.si_use_fast(hi, wi, k):
                     y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack_fast(kcrs), k)
                 elif (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
                     y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack3x3(kcrs), k)
@@ -464,6 +468,15 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
                 if np.any(step.bias != 0):
                     y = y + bias.view(1, -1, 1, 1)
                     sparse = False
+            elif variant == VARIANT_SPARSE_FILTER:
+                # the strategy I / II layer (layers._sf_layer), all images in one launch
+                nodes, seg, packed = ly._device_bank(step.params)
+                if packed is not None and (step.stride, step.padding) == (1, 1) and not ly._EXACT and \
+                        ly._fast_fills_gpu(dims, k):
+                    y = device.sf_conv3x3(device.to_halo(x), packed, bias, relu=False, pool=False, w=dims[2])
+                    y = device.from_halo(y, dims[2]).contiguous()
+                else:
+                    y = device.sf_conv_exact(x, nodes, seg, k, h_f, w_f, step.stride, step.padding, bias)
             else:
                 y = device.dense_conv_exact(x, kcrs, step.stride, step.padding, bias)
                 if step.fused_pool is not None:

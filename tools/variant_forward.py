@@ -1,8 +1,10 @@
 """Time network.forward for the dense_baseline and sparse_input variants: the batched
 device path (one launch per layer for the whole batch, activations in HBM) against the
 per-image layer path (network._BATCHED = False), and check they agree bit for bit.
+Wall clock per forward call (batched: best of 3).
 
 usage: python tools/variant_forward.py [--kind vgg16_desk] [--scale 1.0] [--hw 224] [--batch 8]
+       [--variants sparse_input,dense_baseline,sparse_filter] [--filter-density 0.1]
 """
 import argparse
 import os
@@ -25,21 +27,29 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--density", type=float, default=0.5)
     ap.add_argument("--variants", default="sparse_input,dense_baseline")
+    ap.add_argument("--filter-density", type=float, default=0.1, help="sparse_filter weights kept")
     args = ap.parse_args()
     for variant in args.variants.split(","):
         net = nw.build_benchmark_net(args.kind, args.scale, input_hw=args.hw, variant=variant)
-        prepared = nw.prepare(net, nw.random_weights(net, 7))
+        weights = nw.random_weights(net, 7)
+        if variant == "sparse_filter":
+            weights = nw.prune_weights(weights, args.filter_density, 7)
+        prepared = nw.prepare(net, weights)
         xs = [fs.prune_random(nw.random_input(net.input_dims, 100 + i), args.density, 100 + i)
               for i in range(args.batch)]
         inp = [fs.sparsify_tensor3(x, fs.AxisOrder3.CHW) if variant == "sparse_input" else x for x in xs]
-        nw.forward(prepared, inp[:1])  # warm-up (allocations, library load)
-        t0 = time.perf_counter()
-        a = nw.forward(prepared, inp).outputs
-        t_b = time.perf_counter() - t0
+        def best(reps=3):
+            t, out = 1e30, None
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                out = nw.forward(prepared, inp).outputs
+                t = min(t, time.perf_counter() - t0)
+            return t, out
+
+        nw.forward(prepared, inp)  # warm-up (allocations, library load)
+        t_b, a = best()
         nw._BATCHED = False
-        t0 = time.perf_counter()
-        b = nw.forward(prepared, inp).outputs
-        t_s = time.perf_counter() - t0
+        t_s, b = best(1)
         nw._BATCHED = True
         same = all((x.nodes.tobytes() == y.nodes.tobytes()) if isinstance(x, fs.SparseTensor3)
                    else np.array_equal(np.asarray(x.data).view(np.int32), np.asarray(y.data).view(np.int32))
