@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import math
 import struct
+import threading
 import time
 from dataclasses import dataclass, replace
 
@@ -331,6 +332,10 @@ class _Staging:
 
 
 _staging = _Staging()
+# forward() may be called from several host threads (the reference's kernels are nogil
+# and its API thread-safe); the engine's device buffers and the pinned staging above are
+# shared per process, so engine forwards are serialised.
+_engine_lock = threading.Lock()
 
 
 def pinned_batch(n: int, dims) -> list:
@@ -572,7 +577,8 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
     densities = [[] for _ in range(prepared.n_layers)] if record_density else None
     t0 = time.perf_counter()
     if prepared.engine is not None and not record_density:
-        outputs = _forward_engine(prepared, batch)
+        with _engine_lock:
+            outputs = _forward_engine(prepared, batch)
     elif _BATCHED and _batched_inputs_ok(prepared, batch):
         outputs = _forward_batched(prepared, batch, densities)
     else:
