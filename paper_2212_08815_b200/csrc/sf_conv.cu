@@ -385,12 +385,21 @@ __global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
         if (!p.pool) {
             // halo-column layout: logical column x lives at memory column x + 1
             float *dst = p.y + (((int64_t)img * p.k + k) * p.h + y0) * p.ldo + x0 + 1;
+            const bool full_row = x0 + TILE <= p.w;
 #pragma unroll
             for (int py = 0; py < TILE; ++py) {
                 if (y0 + py >= p.h) break;
+                float *d = dst + (int64_t)py * p.ldo;
+                if (full_row) {
+                    // memory columns x0+1 .. x0+4: the middle pair is 8-byte aligned
+                    d[0] = o[py][0];
+                    *reinterpret_cast<float2 *>(d + 1) = make_float2(o[py][1], o[py][2]);
+                    d[3] = o[py][3];
+                } else {
 #pragma unroll
-                for (int px = 0; px < TILE; ++px)
-                    if (x0 + px < p.w) dst[(int64_t)py * p.ldo + px] = o[py][px];
+                    for (int px = 0; px < TILE; ++px)
+                        if (x0 + px < p.w) d[px] = o[py][px];
+                }
             }
         } else {
             // fused 2x2/2 max-pool: output (h/2, w/2) with row pitch ldo
