@@ -293,3 +293,27 @@ def test_full_size_vgg16_config3_against_oracle(oracle):
     for st, (nodes, seg, k, _) in zip(eng.steps, banks):
         mults += oracle.sf_count(st.h, st.w, seg, len(nodes), k, 3, 3, 1, 1)
     assert eng.flops_per_image() == 2 * mults
+
+
+def test_full_size_config5_batch_invariance(oracle):
+    """BASELINE config 5 at full size (batch 256, 224x224, 95% zeros): a batch-sharded
+    run is only correct if an image's output does not depend on its batch neighbours or
+    position -- images 0, 137 and 255 of the 256-image pass equal their batch-1 passes
+    bit for bit; image 0 against the oracle (normwise)."""
+    import torch
+
+    from paper_2212_08815_b200.engine import VGGEngine
+
+    layers = wl.vgg16_weights(seed=103, zero_frac=0.95)
+    x = torch.from_numpy(wl.vgg16_input(256, seed=105)).cuda()
+    eng = VGGEngine(layers, batch=256, hw=224)
+    y = eng.forward_device(x).clone()
+    for i in (0, 137, 255):
+        yi = eng.forward_device(x[i : i + 1].contiguous())
+        assert torch.equal(y[i : i + 1].view(torch.int32), yi.view(torch.int32)), i
+    banks = []
+    for wt, b in layers:
+        nodes, seg = oracle.encode_bank(wt)
+        banks.append((nodes, seg, wt.shape[0], b))
+    ref = oracle.vgg_forward(x[:1].cpu().numpy(), banks)
+    assert normwise_err(y[:1].cpu().numpy(), ref) <= TOL
