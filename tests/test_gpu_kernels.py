@@ -364,3 +364,25 @@ def test_pool_relu_and_layouts(dev):
         assert np.array_equal(hn[..., 1 : w + 1], x), shape
         assert not hn[..., 0].any() and not hn[..., w + 1 :].any(), shape
         assert np.array_equal(dev.halo_to_whc(hal, w).cpu().numpy(), x.transpose(0, 3, 2, 1)), shape
+
+
+@pytest.mark.parametrize("layer,zf", [(8, 0.9), (5, 0.5), (1, 0.75)])
+def test_si_fast_at_vgg_layer_size(dev, layer, zf):
+    """BASELINE config 4 shapes (batch 4): the channel-major SI kernel against the
+    bit-exact strip kernel (itself pinned to the reference), north-star tolerance; and
+    linearity in the weights (W1 + W2 applied = the two results added, to fp32
+    reassociation)."""
+    import torch
+
+    x, wt, _ = wl.sweep_layer(layer, "si", zf, n=4)
+    n, c, h, w = x.shape
+    k = wt.shape[0]
+    enc = dev.encode_order(_t(x), "CHW")
+    ref = dev.si_conv3x3(enc.nodes, enc.seg_off, n, c, h, w, dev.si_pack3x3(_t(wt)), k)
+    got = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, dev.si_pack_fast(_t(wt)), k)
+    assert normwise_err(got.cpu().numpy(), ref.cpu().numpy()) <= FAST_TOL
+    w2 = np.random.default_rng(layer).normal(0, 0.05, wt.shape).astype(np.float32)
+    a = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, dev.si_pack_fast(_t(w2)), k)
+    s = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, dev.si_pack_fast(_t(wt + w2)), k)
+    assert normwise_err(s.cpu().numpy(), (got + a).cpu().numpy()) <= FAST_TOL
+    torch.cuda.synchronize()
