@@ -20,6 +20,12 @@ def main():
     ref, ref5 = load("r01_bench_reference.json"), load("r01_bench_reference_c5.json")
     c12, c4 = load("r01_configs_12.json"), load("r01_c4_sweep.json")
     step_tf = c3["nnz_gflops"] / 1e3 if "nnz_gflops" in c3 else None
+    sweep = {}
+    with open(os.path.join(ROOT, "profiles", "r01_batch_sweep.txt")) as fh:
+        for line in fh:
+            if line.startswith("batch "):
+                f = line.split()
+                sweep[int(f[1])] = (float(f[6]), float(f[8]))  # ms/step, img/s
     sf = {z: c4_ranges(c4, "sf", z) for z in (0.5, 0.75, 0.9, 0.95, 0.99)}
     si = {z: c4_ranges(c4, "si", z) for z in (0.5, 0.9)}
     sif = {z: c4_ranges(c4, "si_fast", z) for z in (0.5, 0.9)}
@@ -37,6 +43,7 @@ reference path (`oracle/`, OpenMP) on the same box's {c3["cpu_baseline"]["cores"
 | C2: SI 128→128 @28², 90% input zeros, N=1 | strip kernel (shared-memory weights) on device nodes | {c12["c2_kernel"]["us_per_call_graph"]:.1f} µs = {c12["c2_kernel"]["nnz_gflops"]:.0f} nnz-GFLOP/s (bit-exact) | `profiles/r01_configs_12.json` |
 | C2 | GPU encoder + kernel (incl. the node-count sync) | {c12["c2_encode_plus_kernel"]["us_per_call"]:.0f} µs; vs the reference on CPU (1 thread, §2.2): 78.8 ms | same |
 | C3: VGG16 @224², 90% zeros, batch 32 | images/s, inputs in HBM (`value`) | {c3["value"]:.0f} img/s ({c3["ms_per_step"]:.2f} ms/step = {c3["nnz_gflops"] / 1e3:.1f} nnz-TFLOP/s over the step); the kernel's launches average {c3["roofline"]["achieved"]:.2f} nnz-TFLOP/s = {100 * c3["roofline"]["frac"]:.1f} % of FP32 peak; DRAM {c3["roofline"]["traffic"] / 1e6:.0f} MB per layer vs {c3["roofline"]["algorithmic_bytes_per_launch"] / 1e6:.0f} MB algorithmic | `profiles/r01_bench_c3.json`, `profiles/r01_bench_launches_summary.json` |
+| C3, batch 1 (latency) | device time per image, input in HBM | {sweep[1][0]:.2f} ms ({sweep[1][1]:.0f} img/s); batch 4: {sweep[4][1]:.0f} img/s, 8: {sweep[8][1]:.0f}, 16: {sweep[16][1]:.0f}, 64: {sweep[64][1]:.0f} | `profiles/r01_batch_sweep.txt` |
 | C3 | images/s through `network.forward` with host buffers (`e2e`) | {c3["e2e"]["value"]:.0f} img/s (inputs in pinned memory); {c3["e2e"]["pageable"]["value"]:.0f} with pageable numpy inputs | same |
 | C3 | reference CPU path (oracle port, {c3["cpu_baseline"]["cores"]} threads, {c3["cpu_baseline"]["sample"].split(",")[0]}) | {c3["cpu_baseline"]["value"]:.2f} img/s → GPU e2e ×{c3["e2e"]["value"] / c3["cpu_baseline"]["value"]:.0f} | same, `profiles/r01_bench_reference.json` ({ref["value"]:.2f} img/s) |
 | C4: 13 layers × SF {{50,75,90,95,99}} % / SI {{50,75,90,95}} %, batch 32 | nnz-TFLOP/s per layer (L1–L12; L0 has 3 input channels) | SF 50 %: {sf[0.5]}, 75 %: {sf[0.75]}, 90 %: {sf[0.9]}, 95 %: {sf[0.95]}, 99 %: {sf[0.99]}; SI channel-major kernel 50 %: {sif[0.5]}, 90 %: {sif[0.9]} (the bit-exact strip kernel: {si[0.5]} / {si[0.9]}); normwise error of the channel-major kernel vs the exact one ≤ {max(r.get("normwise_err_vs_exact", 0) for r in c4):.1e} | `profiles/r01_c4_sweep.json` |
