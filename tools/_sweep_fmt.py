@@ -1,3 +1,7 @@
+"""Compact one-line-per-point view of tools/sweep_c4.py JSON lines (stdin).
+
+usage: python tools/sweep_c4.py ... | python tools/_sweep_fmt.py
+"""
 import sys,json
 for l in sys.stdin:
     try: r=json.loads(l)
