@@ -154,7 +154,7 @@ int fscnn_dense_conv_exact(const float *x, int n, int c, int h, int w, const flo
  * [K][C][3][3] bank (itself decoded from the reference's CHW SparseTensor4 by
  * fscnn_decode, or straight from dense weights).
  * ------------------------------------------------------------------------- */
-int fscnn_sf_pack_kt(void); /* default filters per group (the kernel supports kt = 4 and 8) */
+int fscnn_sf_pack_kt(void); /* default filters per group (the kernel supports kt = 2, 4 and 8) */
 int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *seg_off,
                           int64_t *total_nodes, void *workspace, size_t workspace_bytes,
                           void *stream);

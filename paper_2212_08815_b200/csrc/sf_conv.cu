@@ -100,15 +100,18 @@ __global__ void dense_exact_kernel(const float *__restrict__ x, int c_n, int h_i
 // ------------------------------------------------------------------------------
 // fast 3x3 kernel
 // ------------------------------------------------------------------------------
-// KT filters per warp (4 or 8, == the pack's kt); a CTA always holds 32 filters:
-// KT=4 -> 8 warps (<=128 regs, 2 CTAs = 16 warps/SM), KT=8 -> 4 warps (2 CTAs = 8 warps/SM)
+// KT filters per warp (2, 4 or 8, == the pack's kt); a CTA holds 32 filters for KT = 4
+// (8 warps, <=128 regs, 2 CTAs = 16 warps/SM) and 8 (4 warps), 16 for KT = 2 (8 warps:
+// twice the CTAs and half the nonzeros per warp, for layers whose KT = 4 grid cannot fill
+// the GPU -- small batches).  Each filter's accumulation order (channels ascending, then
+// its taps ascending) does not depend on KT, so the results are bit-identical.
 #ifndef FSCNN_SF3_CTA_FILTERS
 #define FSCNN_SF3_CTA_FILTERS 32
 #endif
 constexpr int CTA_FILTERS = FSCNN_SF3_CTA_FILTERS;
 constexpr int CTAS_PER_SM = CTA_FILTERS == 32 ? 2 : 1;
 template <int KT> struct SfCfg {
-    static constexpr int NWARP = CTA_FILTERS / KT;
+    static constexpr int NWARP = KT == 2 ? 8 : CTA_FILTERS / KT;
     static constexpr int NTHREADS = NWARP * 32;
 };
 constexpr int MAX_STAGES = 4;
@@ -595,6 +598,9 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
         case 8 * 16 + 8: return launch_sf3x3<8, 8>(map, p, st);
         case 4 * 16 + 8: return launch_sf3x3<4, 8>(map, p, st);
         case 2 * 16 + 8: return launch_sf3x3<2, 8>(map, p, st);
+        case 8 * 16 + 2: return launch_sf3x3<8, 2>(map, p, st);
+        case 4 * 16 + 2: return launch_sf3x3<4, 2>(map, p, st);
+        case 2 * 16 + 2: return launch_sf3x3<2, 2>(map, p, st);
         default: set_error("unsupported sub-region height %d / kt %d", ly, kt); return FSCNN_ERR_ARG;
     }
 }

@@ -170,7 +170,7 @@ SMEM_2CTA = 113 * 1024  # per-CTA budget that keeps two CTAs resident per SM
 
 
 def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4, stages: int = STAGES) -> int:
-    NWARP = CTA_FILTERS // kt
+    NWARP = 8 if kt == 2 else CTA_FILTERS // kt  # mirrors SfCfg in sf_conv.cu
     li, box = 8 // ly, _align(BOXW * (TILE * ly + 2) * cc, 32)
     n_chunks = math.ceil(c / cc)
     return (stages * li * box * 4 + stages * NWARP * ent_cap * 8 + 2 * stages * 8
@@ -183,6 +183,22 @@ def pick_ly(c: int, h: int) -> int:
     56/28/14, where they pad more rows than 8x16); 8x16 for shallow inputs (c < 8) and
     short images."""
     return 2 if (c < 8 or h <= 8) else 4
+
+
+def sf_ctas(n: int, h: int, w: int, k: int, ly: int, kt: int) -> int:
+    """CTAs of one fast sparse-filter launch (mirrors launch_sf3x3 in sf_conv.cu)."""
+    li = 8 // ly
+    n_sub = n * -(-h // (TILE * ly)) * -(-w // SUBW)
+    filters_per_cta = 16 if kt == 2 else CTA_FILTERS
+    return -(-n_sub // li) * -(-k // filters_per_cta)
+
+
+def sf_small_grid(n: int, h: int, w: int, k: int, ly: int) -> bool:
+    """True when the 4-filters-per-warp grid cannot give every SM a CTA (batch-1 deep
+    layers): there the 2-filters-per-warp kernel (twice the CTAs, half the nonzeros per
+    warp, bit-identical results) is faster -- measured 213 -> 157 us on VGG16 layer 8
+    at batch 1, and slower once the grid fills the GPU (tools/kt_check.py)."""
+    return sf_ctas(n, h, w, k, ly, 4) < 148
 
 
 @dataclass
@@ -235,7 +251,7 @@ def default_kt(c: int) -> int:
     import os
 
     forced = int(os.environ.get("FSCNN_SF3_KT", "0"))
-    return forced if forced in (4, 8) else int(_lib.load().fscnn_sf_pack_kt())
+    return forced if forced in (2, 4, 8) else int(_lib.load().fscnn_sf_pack_kt())
 
 
 def sf_pack(w_kc33: torch.Tensor, kt: int | None = None) -> PackedBank:

@@ -41,6 +41,14 @@ class ConvStep:
     matrix_off: torch.Tensor
     n_nodes: int
     ly: int = 0
+    bank2: device.PackedBank | None = None  # 2 filters per warp, for grids too small to fill the GPU
+
+    def bank_for(self, n: int) -> device.PackedBank:
+        """The packed stream for a launch over n images: KT = 2 when the KT = 4 grid
+        leaves SMs idle (bit-identical results either way)."""
+        if self.bank2 is not None and device.sf_small_grid(n, self.h, self.w, self.k, self.ly):
+            return self.bank2
+        return self.bank
 
 
 def _align4(v: int) -> int:
@@ -81,8 +89,9 @@ class VGGEngine:
                 bias_t = torch.as_tensor(np.asarray(bias_np, np.float32) if not torch.is_tensor(bias_np) else bias_np)
                 bias_t = bias_t.to(dev, torch.float32).contiguous()
             bank = device.sf_pack(dense)
+            bank2 = device.sf_pack(dense, 2) if bank.kt == 4 else None
             self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes,
-                                       device.pick_ly(c, h)))
+                                       device.pick_ly(c, h), bank2))
             c = k
             if pool:
                 h //= 2
@@ -143,8 +152,9 @@ class VGGEngine:
             with torch.cuda.stream(s):
                 cur, w = xin[lo:hi], w0
                 for st, out in zip(self.steps[first:], bufs[first:]):
-                    device.sf_conv3x3(cur, st.bank, st.bias, relu=True, pool=st.pool, out=out[lo:hi], w=w,
-                                      ly=st.ly)
+                    # the parts run concurrently: the grid that must fill the GPU is the batch's
+                    device.sf_conv3x3(cur, st.bank_for(n), st.bias, relu=True, pool=st.pool, out=out[lo:hi],
+                                      w=w, ly=st.ly)
                     cur = out[lo:hi]
                     w = w // 2 if st.pool else w
         for s in streams:
@@ -192,7 +202,7 @@ class VGGEngine:
             cur.wait_event(ev)
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
-            device.sf_conv3x3(self._in[lo:hi], first.bank, first.bias, relu=True, pool=first.pool,
+            device.sf_conv3x3(self._in[lo:hi], first.bank_for(n), first.bias, relu=True, pool=first.pool,
                               out=bufs[0][lo:hi], w=self.hw, ly=first.ly)
         return device.halo_to_whc(self._run_from(1, bufs[0]), self.out_hw)
 

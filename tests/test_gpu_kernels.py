@@ -158,6 +158,26 @@ def test_sf_fast_matches_oracle(dev, oracle, n, c, k, h, w, zf, ly):
         assert normwise_err(dev.from_halo(yp, w // 2).cpu().numpy(), want) <= FAST_TOL
 
 
+@pytest.mark.parametrize("k", [36, 64, 8])
+def test_sf_fast_filters_per_warp_agree_bitwise(dev, k):
+    """2, 4 or 8 filters per warp only regroup the filters: bit-identical outputs (the
+    engine picks KT = 2 for grids that cannot fill the GPU)."""
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((2, 24, 28, 28)).astype(np.float32)
+    wt = rng.standard_normal((k, 24, 3, 3)).astype(np.float32)
+    wt[rng.random(wt.shape) < 0.9] = 0
+    bias = rng.standard_normal(k).astype(np.float32)
+    xp = dev.to_halo(_t(x))
+    outs = []
+    for kt in (2, 4, 8):
+        bank = dev.sf_pack(_t(wt), kt)
+        for pool in (False, True):
+            outs.append((kt, pool, dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=28).cpu().numpy()))
+    for kt, pool, o in outs:
+        ref = [q for kk, pp, q in outs if kk == 4 and pp == pool][0]
+        assert o.tobytes() == ref.tobytes(), (kt, pool)
+
+
 @pytest.mark.parametrize("n,h,w", [(3, 28, 28), (2, 56, 56), (5, 14, 14), (2, 27, 30)])
 def test_sf_fast_layouts_agree_bitwise(dev, n, h, w):
     """Every sub-region height runs the same per-lane arithmetic: bit-identical outputs."""
