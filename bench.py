@@ -289,7 +289,8 @@ def main():
         for i, (st, out) in enumerate(zip(eng.steps, bufs)):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            pdev.sf_conv3x3(cur, st.bank_for(n_local), st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly)
+            bank, warps = st.plan_for(n_local)
+            pdev.sf_conv3x3(cur, bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly, cta_warps=warps)
             b.record()
             b.synchronize()
             layer_ms[i] += a.elapsed_time(b) / reps

@@ -110,9 +110,10 @@ __global__ void dense_exact_kernel(const float *__restrict__ x, int c_n, int h_i
 #endif
 constexpr int CTA_FILTERS = FSCNN_SF3_CTA_FILTERS;
 constexpr int CTAS_PER_SM = CTA_FILTERS == 32 ? 2 : 1;
+// Default warps per CTA for KT; a launch may ask for 4-warp CTAs with KT = 2 (8 filters
+// per CTA) when even the 16-filter grid leaves most SMs idle.
 template <int KT> struct SfCfg {
     static constexpr int NWARP = KT == 2 ? 8 : CTA_FILTERS / KT;
-    static constexpr int NTHREADS = NWARP * 32;
 };
 constexpr int MAX_STAGES = 4;
 constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
@@ -201,11 +202,11 @@ struct Sf3Params {
                               // 8 = no epilogue stores
 };
 
-template <int LY, int KT>
-__global__ void __launch_bounds__(SfCfg<KT>::NTHREADS, CTAS_PER_SM)
+template <int LY, int KT, int NW>
+__global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
     sf3x3_kernel(const __grid_constant__ CUtensorMap tmap, const Sf3Params p) {
-    constexpr int NWARP = SfCfg<KT>::NWARP;
-    constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
+    constexpr int NWARP = NW;
+    constexpr int NTHREADS = NW * 32;
     constexpr int LI = 8 / LY;          // sub-regions per CTA
     constexpr int SUBH = TILE * LY;     // sub-region height
     constexpr int BOXH = SUBH + 2;
@@ -453,7 +454,7 @@ EncodeTiledFn get_encode_tiled() {
     return fn;
 }
 
-template <int LY, int KT>
+template <int LY, int KT, int NW = SfCfg<KT>::NWARP>
 int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     constexpr int LI = 8 / LY;
     constexpr int SUBH = TILE * LY;
@@ -463,8 +464,8 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
     p.box_floats = BOXW * (SUBH + 2) * p.cc;
     // each box must start 128-byte aligned (TMA destination)
     p.box_floats = (p.box_floats + 31) & ~31;
-    constexpr int NWARP = SfCfg<KT>::NWARP;
-    constexpr int NTHREADS = SfCfg<KT>::NTHREADS;
+    constexpr int NWARP = NW;
+    constexpr int NTHREADS = NW * 32;
     const int n_chunks = (int)ceil_div(p.c, p.cc);
     auto smem_for = [&](int st) {
         return (size_t)st * LI * p.box_floats * 4 + (size_t)st * NWARP * p.ent_cap * 8 + 2 * st * 8 +
@@ -479,7 +480,7 @@ int launch_sf3x3(const CUtensorMap &map, Sf3Params &p, cudaStream_t st) {
         set_error("sf3x3: %zu bytes of shared memory needed; lower cc", smem);
         return FSCNN_ERR_UNSUPPORTED;
     }
-    auto kern = sf3x3_kernel<LY, KT>;
+    auto kern = sf3x3_kernel<LY, KT, NW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("sf3x3: smem attribute (%zu bytes): %s", smem, cudaGetErrorString(e));
@@ -591,6 +592,18 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
         return FSCNN_ERR_CUDA;
     }
     cudaStream_t st = as_stream(stream);
+    // kt: filters per warp in the low byte (== the pack's kt); bits 8-15: warps per CTA
+    // (0 = default; 4 with kt = 2 for very small grids)
+    const int cta_warps = (kt >> 8) & 0xff;
+    kt &= 0xff;
+    if (kt == 2 && cta_warps == 4) {
+        switch (ly) {
+            case 8: return launch_sf3x3<8, 2, 4>(map, p, st);
+            case 4: return launch_sf3x3<4, 2, 4>(map, p, st);
+            case 2: return launch_sf3x3<2, 2, 4>(map, p, st);
+            default: break;
+        }
+    }
     switch (ly * 16 + kt) {
         case 8 * 16 + 4: return launch_sf3x3<8, 4>(map, p, st);
         case 4 * 16 + 4: return launch_sf3x3<4, 4>(map, p, st);

@@ -189,16 +189,21 @@ def sf_ctas(n: int, h: int, w: int, k: int, ly: int, kt: int) -> int:
     """CTAs of one fast sparse-filter launch (mirrors launch_sf3x3 in sf_conv.cu)."""
     li = 8 // ly
     n_sub = n * -(-h // (TILE * ly)) * -(-w // SUBW)
-    filters_per_cta = 16 if kt == 2 else CTA_FILTERS
+    filters_per_cta = 16 if kt == 2 else CTA_FILTERS  # default warps per CTA
     return -(-n_sub // li) * -(-k // filters_per_cta)
 
 
-def sf_small_grid(n: int, h: int, w: int, k: int, ly: int) -> bool:
-    """True when the 4-filters-per-warp grid cannot give every SM a CTA (batch-1 deep
-    layers): there the 2-filters-per-warp kernel (twice the CTAs, half the nonzeros per
-    warp, bit-identical results) is faster -- measured 213 -> 157 us on VGG16 layer 8
-    at batch 1, and slower once the grid fills the GPU (tools/kt_check.py)."""
-    return sf_ctas(n, h, w, k, ly, 4) < 148
+def sf_grid_plan(n: int, h: int, w: int, k: int, ly: int) -> tuple[int, int]:
+    """(filters per warp, warps per CTA; 0 = default) for a launch over n images.  When
+    the 4-filters-per-warp grid cannot give every SM a CTA (deep layers at small
+    batch), 2 filters per warp (twice the CTAs, half the nonzeros per warp; bit-identical
+    results) are faster, and 4-warp CTAs of those when even that grid is under one CTA
+    per SM: VGG16 layer 8 at batch 1 213 -> 157 -> 142 us; both lose once the grid fills
+    the GPU (tools/kt_check.py)."""
+    g4 = sf_ctas(n, h, w, k, ly, 4)
+    if g4 >= 148:
+        return 4, 0
+    return (2, 0) if 2 * g4 >= 148 else (2, 4)
 
 
 @dataclass
@@ -304,7 +309,7 @@ def from_halo(xh: torch.Tensor, w: int) -> torch.Tensor:
 
 def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, relu: bool,
                pool: bool, out: torch.Tensor | None = None, w: int | None = None,
-               ly: int = 0) -> torch.Tensor:
+               ly: int = 0, cta_warps: int = 0) -> torch.Tensor:
     """Fast 3x3/s1/p1 sparse-filter conv (+ReLU, +fused 2x2 max-pool).
 
     ``x`` is a halo-column buffer [N, C, H, pitch] (see halo_pitch) holding a logical
@@ -324,7 +329,8 @@ def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, rel
         out = halo_empty(n, bank.k, ho, wo, x.device)
     ldo = int(out.stride(2))
     call("fscnn_sf_conv3x3_ex", ptr(x), n, c, h, w, ldi, ptr(bank.nodes), ptr(bank.seg_off),
-         bank.total, mx, cc, bank.k, ptr(bias), int(relu), int(pool), ptr(out), ldo, ly, bank.kt, stream())
+         bank.total, mx, cc, bank.k, ptr(bias), int(relu), int(pool), ptr(out), ldo, ly,
+         bank.kt | (int(cta_warps) << 8), stream())
     return out
 
 

@@ -43,12 +43,14 @@ class ConvStep:
     ly: int = 0
     bank2: device.PackedBank | None = None  # 2 filters per warp, for grids too small to fill the GPU
 
-    def bank_for(self, n: int) -> device.PackedBank:
-        """The packed stream for a launch over n images: KT = 2 when the KT = 4 grid
-        leaves SMs idle (bit-identical results either way)."""
-        if self.bank2 is not None and device.sf_small_grid(n, self.h, self.w, self.k, self.ly):
-            return self.bank2
-        return self.bank
+    def plan_for(self, n: int) -> tuple[device.PackedBank, int]:
+        """(packed stream, warps per CTA) for a launch over n images: 2 filters per warp
+        when the 4-filter grid leaves SMs idle (bit-identical results either way)."""
+        if self.bank2 is not None:
+            kt, warps = device.sf_grid_plan(n, self.h, self.w, self.k, self.ly)
+            if kt == 2:
+                return self.bank2, warps
+        return self.bank, 0
 
 
 def _align4(v: int) -> int:
@@ -153,8 +155,9 @@ class VGGEngine:
                 cur, w = xin[lo:hi], w0
                 for st, out in zip(self.steps[first:], bufs[first:]):
                     # the parts run concurrently: the grid that must fill the GPU is the batch's
-                    device.sf_conv3x3(cur, st.bank_for(n), st.bias, relu=True, pool=st.pool, out=out[lo:hi],
-                                      w=w, ly=st.ly)
+                    bank, warps = st.plan_for(n)
+                    device.sf_conv3x3(cur, bank, st.bias, relu=True, pool=st.pool, out=out[lo:hi], w=w, ly=st.ly,
+                                      cta_warps=warps)
                     cur = out[lo:hi]
                     w = w // 2 if st.pool else w
         for s in streams:
@@ -202,8 +205,9 @@ class VGGEngine:
             cur.wait_event(ev)
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
-            device.sf_conv3x3(self._in[lo:hi], first.bank_for(n), first.bias, relu=True, pool=first.pool,
-                              out=bufs[0][lo:hi], w=self.hw, ly=first.ly)
+            bank, warps = first.plan_for(n)
+            device.sf_conv3x3(self._in[lo:hi], bank, first.bias, relu=True, pool=first.pool,
+                              out=bufs[0][lo:hi], w=self.hw, ly=first.ly, cta_warps=warps)
         return device.halo_to_whc(self._run_from(1, bufs[0]), self.out_hw)
 
     def forward_device(self, x: torch.Tensor) -> torch.Tensor:

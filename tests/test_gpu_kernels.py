@@ -169,13 +169,14 @@ def test_sf_fast_filters_per_warp_agree_bitwise(dev, k):
     bias = rng.standard_normal(k).astype(np.float32)
     xp = dev.to_halo(_t(x))
     outs = []
-    for kt in (2, 4, 8):
+    for kt, warps in ((2, 0), (4, 0), (8, 0), (2, 4)):  # (2, 4): 4-warp CTAs
         bank = dev.sf_pack(_t(wt), kt)
         for pool in (False, True):
-            outs.append((kt, pool, dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=28).cpu().numpy()))
-    for kt, pool, o in outs:
-        ref = [q for kk, pp, q in outs if kk == 4 and pp == pool][0]
-        assert o.tobytes() == ref.tobytes(), (kt, pool)
+            y = dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=28, cta_warps=warps)
+            outs.append(((kt, warps), pool, y.cpu().numpy()))
+    for cfg, pool, o in outs:
+        ref = [q for kk, pp, q in outs if kk == (4, 0) and pp == pool][0]
+        assert o.tobytes() == ref.tobytes(), (cfg, pool)
 
 
 @pytest.mark.parametrize("n,h,w", [(3, 28, 28), (2, 56, 56), (5, 14, 14), (2, 27, 30)])

@@ -31,10 +31,10 @@ def main():
         bias = torch.from_numpy(b).cuda()
         wd = torch.from_numpy(wt).cuda()
         res, outs = [], []
-        for kt in (4, 2, 8):
+        for kt, cw in ((4, 0), (2, 0), (8, 0), (2, 4)):
             bank = device.sf_pack(wd, kt)
             out = device.halo_empty(args.batch, k, h, w)
-            fn = lambda: device.sf_conv3x3(xh, bank, bias, True, False, out=out, w=w)
+            fn = lambda: device.sf_conv3x3(xh, bank, bias, True, False, out=out, w=w, cta_warps=cw)
             fn()
             torch.cuda.synchronize()
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,7 +43,7 @@ def main():
                 fn()
             e.record()
             e.synchronize()
-            res.append((kt, a.elapsed_time(e) / args.reps * 1e3))
+            res.append((f"{kt}" + ("/4w" if cw else ""), a.elapsed_time(e) / args.reps * 1e3))
             outs.append(out.clone())
         same = all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs[1:])
         print(f"L{li} {c}->{k} @{h} batch {args.batch}: " + ", ".join(f"kt{kt} {us:.1f} us" for kt, us in res)
