@@ -154,7 +154,7 @@ int fscnn_dense_conv_exact(const float *x, int n, int c, int h, int w, const flo
  * [K][C][3][3] bank (itself decoded from the reference's CHW SparseTensor4 by
  * fscnn_decode, or straight from dense weights).
  * ------------------------------------------------------------------------- */
-int fscnn_sf_pack_kt(void); /* default filters per group (the kernel supports kt = 2, 4 and 8) */
+int fscnn_sf_pack_kt(void); /* default filters per group (the kernel supports kt = 1, 2, 4 and 8) */
 int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *seg_off,
                           int64_t *total_nodes, void *workspace, size_t workspace_bytes,
                           void *stream);
@@ -167,8 +167,8 @@ int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, int kt, const int64_t
  * aligned ranges).  max_chunk_entries: the largest node count (sentinels included)
  * of any group over any run of `cc` consecutive channels.  ly selects the
  * sub-region height 4*ly (8, 4 or 2; 0 = by h).  kt: the stream's filters per group
- * (2, 4 or 8) in the low byte; bits 8-15 may ask for 4-warp CTAs with kt = 2 (small
- * grids; 0 = default 8 warps) -- the results do not depend on either.  relu applies
+ * (1, 2, 4 or 8) in the low byte; bits 8-15 may ask for 4-warp CTAs with kt = 2 (small
+ * grids; 0 = default: 8 warps, 4 for kt = 1) -- the results do not depend on either.  relu applies
  * np.maximum(.,0) before the pool, as the reference's conv -> relu -> pool sequence
  * does. */
 int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,

@@ -614,7 +614,7 @@ int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *se
                           int64_t *total_nodes, void *workspace, size_t workspace_bytes,
                           void *stream) {
     FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && total_nodes, "bad pack arguments");
-    FSCNN_REQUIRE(kt == 2 || kt == 4 || kt == 8, "kt must be 2, 4 or 8");
+    FSCNN_REQUIRE(kt == 1 || kt == 2 || kt == 4 || kt == 8, "kt must be 1, 2, 4 or 8");
     int64_t groups = ceil_div(k, kt);
     SfPackSrc src{w_kc33, k, c, kt, (int64_t)kt * 9};
     return encode_offsets_impl(src, groups * c, false, seg_off, total_nodes, workspace,
@@ -624,7 +624,7 @@ int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *se
 int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, int kt, const int64_t *seg_off,
                         int64_t total_nodes, fscnn_node *nodes, void *stream) {
     FSCNN_REQUIRE(k > 0 && c > 0 && w_kc33 && seg_off && nodes, "bad pack arguments");
-    FSCNN_REQUIRE(kt == 2 || kt == 4 || kt == 8, "kt must be 2, 4 or 8");
+    FSCNN_REQUIRE(kt == 1 || kt == 2 || kt == 4 || kt == 8, "kt must be 1, 2, 4 or 8");
     int64_t groups = ceil_div(k, kt);
     SfPackSrc src{w_kc33, k, c, kt, (int64_t)kt * 9};
     cudaStream_t st = as_stream(stream);

@@ -191,8 +191,8 @@ def emit(KT: int) -> None:
 def main():
     print("// GENERATED by gen_sf3x3_dispatch.py -- do not edit by hand.")
     print("// One staged chunk of input channels of the fast sparse-filter kernel (overloads")
-    print("// for KT = 2, 4 and 8 filters per warp); see the generator for the protocol.")
-    for kt in (2, 4, 8):
+    print("// for KT = 1, 2, 4 and 8 filters per warp); see the generator for the protocol.")
+    for kt in (1, 2, 4, 8):
         emit(kt)
 
 

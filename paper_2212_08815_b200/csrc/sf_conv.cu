@@ -100,11 +100,12 @@ __global__ void dense_exact_kernel(const float *__restrict__ x, int c_n, int h_i
 // ------------------------------------------------------------------------------
 // fast 3x3 kernel
 // ------------------------------------------------------------------------------
-// KT filters per warp (2, 4 or 8, == the pack's kt); a CTA holds 32 filters for KT = 4
-// (8 warps, <=128 regs, 2 CTAs = 16 warps/SM) and 8 (4 warps), 16 for KT = 2 (8 warps:
-// twice the CTAs and half the nonzeros per warp, for layers whose KT = 4 grid cannot fill
-// the GPU -- small batches).  Each filter's accumulation order (channels ascending, then
-// its taps ascending) does not depend on KT, so the results are bit-identical.
+// KT filters per warp (1, 2, 4 or 8, == the pack's kt); a CTA holds 32 filters for KT = 4
+// (8 warps, <=128 regs, 2 CTAs = 16 warps/SM) and 8 (4 warps), 16 for KT = 2 (8 warps)
+// and 4 for KT = 1 (4 warps): more CTAs and shorter dispatch chains per warp for layers
+// whose KT = 4 grid cannot fill the GPU (small batches).  Each filter's accumulation
+// order (channels ascending, then its taps ascending) does not depend on KT or the CTA
+// size, so the results are bit-identical.
 #ifndef FSCNN_SF3_CTA_FILTERS
 #define FSCNN_SF3_CTA_FILTERS 32
 #endif
@@ -113,7 +114,7 @@ constexpr int CTAS_PER_SM = CTA_FILTERS == 32 ? 2 : 1;
 // Default warps per CTA for KT; a launch may ask for 4-warp CTAs with KT = 2 (8 filters
 // per CTA) when even the 16-filter grid leaves most SMs idle.
 template <int KT> struct SfCfg {
-    static constexpr int NWARP = KT == 2 ? 8 : CTA_FILTERS / KT;
+    static constexpr int NWARP = KT <= 2 ? (KT == 2 ? 8 : 4) : CTA_FILTERS / KT;
 };
 constexpr int MAX_STAGES = 4;
 constexpr int BOXW = 20;           // smem row pitch (floats) == TMA box width
@@ -601,6 +602,14 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
             case 8: return launch_sf3x3<8, 2, 4>(map, p, st);
             case 4: return launch_sf3x3<4, 2, 4>(map, p, st);
             case 2: return launch_sf3x3<2, 2, 4>(map, p, st);
+            default: break;
+        }
+    }
+    if (kt == 1) {  // 1 filter per warp, 4-warp CTAs: the smallest grids
+        switch (ly) {
+            case 8: return launch_sf3x3<8, 1, 4>(map, p, st);
+            case 4: return launch_sf3x3<4, 1, 4>(map, p, st);
+            case 2: return launch_sf3x3<2, 1, 4>(map, p, st);
             default: break;
         }
     }

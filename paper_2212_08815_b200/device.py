@@ -170,7 +170,7 @@ SMEM_2CTA = 113 * 1024  # per-CTA budget that keeps two CTAs resident per SM
 
 
 def sf3x3_smem_bytes(ly: int, cc: int, ent_cap: int, c: int, kt: int = 4, stages: int = STAGES) -> int:
-    NWARP = 8 if kt == 2 else CTA_FILTERS // kt  # mirrors SfCfg in sf_conv.cu
+    NWARP = {1: 4, 2: 8}.get(kt, CTA_FILTERS // kt)  # mirrors SfCfg in sf_conv.cu
     li, box = 8 // ly, _align(BOXW * (TILE * ly + 2) * cc, 32)
     n_chunks = math.ceil(c / cc)
     return (stages * li * box * 4 + stages * NWARP * ent_cap * 8 + 2 * stages * 8
@@ -189,21 +189,22 @@ def sf_ctas(n: int, h: int, w: int, k: int, ly: int, kt: int) -> int:
     """CTAs of one fast sparse-filter launch (mirrors launch_sf3x3 in sf_conv.cu)."""
     li = 8 // ly
     n_sub = n * -(-h // (TILE * ly)) * -(-w // SUBW)
-    filters_per_cta = 16 if kt == 2 else CTA_FILTERS  # default warps per CTA
+    filters_per_cta = {1: 4, 2: 16}.get(kt, CTA_FILTERS)  # default warps per CTA
     return -(-n_sub // li) * -(-k // filters_per_cta)
 
 
 def sf_grid_plan(n: int, h: int, w: int, k: int, ly: int) -> tuple[int, int]:
     """(filters per warp, warps per CTA; 0 = default) for a launch over n images.  When
-    the 4-filters-per-warp grid cannot give every SM a CTA (deep layers at small
-    batch), 2 filters per warp (twice the CTAs, half the nonzeros per warp; bit-identical
-    results) are faster, and 4-warp CTAs of those when even that grid is under one CTA
-    per SM: VGG16 layer 8 at batch 1 213 -> 157 -> 142 us; both lose once the grid fills
-    the GPU (tools/kt_check.py)."""
+    the 4-filters-per-warp grid cannot give every SM a CTA (deep layers at small batch),
+    fewer filters per warp -- more CTAs, a shorter dispatch chain per warp, more patch
+    reloads per nonzero; bit-identical results -- are faster: 2 per warp below 148 CTAs,
+    1 per warp in 4-warp CTAs at <= 32 (VGG16 layer 8 at batch 1: 213 -> 157 -> 114 us;
+    layer 10: 204 -> 151 -> 96 us); both lose once the grid fills the GPU
+    (tools/kt_check.py)."""
     g4 = sf_ctas(n, h, w, k, ly, 4)
     if g4 >= 148:
         return 4, 0
-    return (2, 0) if 2 * g4 >= 148 else (2, 4)
+    return (2, 0) if g4 > 32 else (1, 4)
 
 
 @dataclass
@@ -256,7 +257,7 @@ def default_kt(c: int) -> int:
     import os
 
     forced = int(os.environ.get("FSCNN_SF3_KT", "0"))
-    return forced if forced in (2, 4, 8) else int(_lib.load().fscnn_sf_pack_kt())
+    return forced if forced in (1, 2, 4, 8) else int(_lib.load().fscnn_sf_pack_kt())
 
 
 def sf_pack(w_kc33: torch.Tensor, kt: int | None = None) -> PackedBank:

@@ -41,15 +41,15 @@ class ConvStep:
     matrix_off: torch.Tensor
     n_nodes: int
     ly: int = 0
-    bank2: device.PackedBank | None = None  # 2 filters per warp, for grids too small to fill the GPU
+    small: dict | None = None  # kt -> packed stream with 1 / 2 filters per warp (small grids)
 
     def plan_for(self, n: int) -> tuple[device.PackedBank, int]:
-        """(packed stream, warps per CTA) for a launch over n images: 2 filters per warp
-        when the 4-filter grid leaves SMs idle (bit-identical results either way)."""
-        if self.bank2 is not None:
+        """(packed stream, warps per CTA) for a launch over n images: fewer filters per
+        warp when the 4-filter grid leaves SMs idle (bit-identical results either way)."""
+        if self.small:
             kt, warps = device.sf_grid_plan(n, self.h, self.w, self.k, self.ly)
-            if kt == 2:
-                return self.bank2, warps
+            if kt in self.small:
+                return self.small[kt], warps
         return self.bank, 0
 
 
@@ -91,9 +91,9 @@ class VGGEngine:
                 bias_t = torch.as_tensor(np.asarray(bias_np, np.float32) if not torch.is_tensor(bias_np) else bias_np)
                 bias_t = bias_t.to(dev, torch.float32).contiguous()
             bank = device.sf_pack(dense)
-            bank2 = device.sf_pack(dense, 2) if bank.kt == 4 else None
+            small = {kt: device.sf_pack(dense, kt) for kt in (1, 2)} if bank.kt == 4 else None
             self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes,
-                                       device.pick_ly(c, h), bank2))
+                                       device.pick_ly(c, h), small))
             c = k
             if pool:
                 h //= 2

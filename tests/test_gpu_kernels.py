@@ -169,7 +169,7 @@ def test_sf_fast_filters_per_warp_agree_bitwise(dev, k):
     bias = rng.standard_normal(k).astype(np.float32)
     xp = dev.to_halo(_t(x))
     outs = []
-    for kt, warps in ((2, 0), (4, 0), (8, 0), (2, 4)):  # (2, 4): 4-warp CTAs
+    for kt, warps in ((2, 0), (4, 0), (8, 0), (2, 4), (1, 0)):  # (2, 4), kt 1: 4-warp CTAs
         bank = dev.sf_pack(_t(wt), kt)
         for pool in (False, True):
             y = dev.sf_conv3x3(xp, bank, _t(bias), relu=True, pool=pool, w=28, cta_warps=warps)

@@ -31,7 +31,7 @@ def main():
         bias = torch.from_numpy(b).cuda()
         wd = torch.from_numpy(wt).cuda()
         res, outs = [], []
-        for kt, cw in ((4, 0), (2, 0), (8, 0), (2, 4)):
+        for kt, cw in ((4, 0), (2, 0), (8, 0), (2, 4), (1, 4)):
             bank = device.sf_pack(wd, kt)
             out = device.halo_empty(args.batch, k, h, w)
             fn = lambda: device.sf_conv3x3(xh, bank, bias, True, False, out=out, w=w, cta_warps=cw)
