@@ -94,8 +94,11 @@ def main():
     enc = device.encode_order(torch.from_numpy(wt).cuda(), "CHW")
     fl = sf_flops(wt, 56, 56)
     fast = lambda: device.sf_conv3x3(xh, bank, bias, False, False, out=out, w=56)
+    kt, warps = device.sf_grid_plan(1, 56, 56, 64, device.pick_ly(64, 56))
+    bank_s = device.sf_pack(torch.from_numpy(wt).cuda(), kt)
+    fast_small = lambda: device.sf_conv3x3(xh, bank_s, bias, False, False, out=out, w=56, cta_warps=warps)
     exact = lambda: device.sf_conv_exact(xd, enc.nodes, enc.seg_off, 64, 3, 3, 1, 1, bias)
-    for name, fn in (("fast", fast), ("exact", exact)):
+    for name, fn in (("fast", fast), ("fast_small_grid", fast_small), ("exact", exact)):
         us, gus = per_call_us(fn), graph_us(fn)
         res[f"c1_{name}"] = {"us_per_call": us, "us_per_call_graph": gus, "nnz_gflop": fl / 1e9,
                              "nnz_gflops": fl / (gus * 1e-6) / 1e9}

@@ -38,7 +38,7 @@ reference path (`oracle/`, OpenMP) on the same box's {c3["cpu_baseline"]["cores"
 
 | Config | Metric | Value | Source |
 |---|---|---|---|
-| C1: SF 64→64 @56², 95% zeros, N=1 | time per layer call (device, graph-launched) | {c12["c1_exact"]["us_per_call_graph"]:.1f} µs = {c12["c1_exact"]["nnz_gflops"]:.0f} nnz-GFLOP/s (reference-order kernel, bit-exact; the tiled fast kernel fills only 16 CTAs here: {c12["c1_fast"]["us_per_call_graph"]:.1f} µs) | `profiles/r01_configs_12.json` |
+| C1: SF 64→64 @56², 95% zeros, N=1 | time per layer call (device, graph-launched) | {c12["c1_exact"]["us_per_call_graph"]:.1f} µs = {c12["c1_exact"]["nnz_gflops"]:.0f} nnz-GFLOP/s (reference-order kernel, bit-exact, what the layer API runs; the tiled fast kernel fills only 16 CTAs here: {c12["c1_fast"]["us_per_call_graph"]:.1f} µs, {c12["c1_fast_small_grid"]["us_per_call_graph"]:.1f} µs with its small-grid plan of 1 filter per warp) | `profiles/r01_configs_12.json` |
 | C1 | vs the reference on CPU (1 thread, §2.2) | 26.5 ms → ×{26500 / c12["c1_exact"]["us_per_call_graph"]:.0f} | §2.2 |
 | C2: SI 128→128 @28², 90% input zeros, N=1 | strip kernel (shared-memory weights) on device nodes | {c12["c2_kernel"]["us_per_call_graph"]:.1f} µs = {c12["c2_kernel"]["nnz_gflops"]:.0f} nnz-GFLOP/s (bit-exact) | `profiles/r01_configs_12.json` |
 | C2 | GPU encoder + kernel (incl. the node-count sync) | {c12["c2_encode_plus_kernel"]["us_per_call"]:.0f} µs; vs the reference on CPU (1 thread, §2.2): 78.8 ms | same |
