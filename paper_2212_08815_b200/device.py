@@ -15,6 +15,7 @@ Tensor conventions
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -158,7 +159,7 @@ def decode_order(nodes, seg_off, dims_bchw, order: str, out: torch.Tensor | None
 STAGES, BOXW, SUBW, TILE = 2, 20, 16, 4  # STAGES: the minimum ring the kernel runs with
 # filters per CTA (CTA_FILTERS // kt warps); must match the library's build
 # (-DFSCNN_SF3_CTA_FILTERS, default 32 = two CTAs per SM, 64 = one)
-CTA_FILTERS = int(__import__("os").environ.get("FSCNN_SF3_CTA_FILTERS", "32"))
+CTA_FILTERS = int(os.environ.get("FSCNN_SF3_CTA_FILTERS", "32"))
 SMEM_LIMIT = 227 * 1024
 
 
@@ -229,8 +230,6 @@ class PackedBank:
             self._cache = {}
         if ly in self._cache:
             return self._cache[ly]
-        import os
-
         forced = int(os.environ.get("FSCNN_SF3_CC", "0"))
         cands = []
         sizes = sorted({16, 8, 4, 2, 1} | ({self.c} if self.c < 16 else set()), reverse=True)
@@ -254,8 +253,6 @@ class PackedBank:
 def default_kt(c: int) -> int:
     """Filters per warp group: 8 halves the per-channel patch reloads (shared-memory
     bound at 4) at half the resident warps; the env var FSCNN_SF3_KT overrides."""
-    import os
-
     forced = int(os.environ.get("FSCNN_SF3_KT", "0"))
     return forced if forced in (1, 2, 4, 8) else int(_lib.load().fscnn_sf_pack_kt())
 
