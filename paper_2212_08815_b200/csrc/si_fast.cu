@@ -11,19 +11,21 @@
 // are bound by that weight stream (16 B of weights per 3 FMAs per lane).  Here the
 // order is free, so each weight is loaded once per (CTA, channel) into registers and
 // reused for every nonzero input of that channel in the tile:
-//   * CTA = NW warps x 32 filters (lane = filter) on one TY x TX output tile of one
-//     image; every lane accumulates the whole tile for its filter in registers.
-//   * per 32-channel chunk the CTA decodes the (TY+2) x (TX+2) input region's node
-//     fibers into shared memory: values [32][region] plus, per channel, a bitmap of the
-//     region positions holding a node (each fiber read as one coalesced 32-node warp
-//     load, cursors kept across chunks).
-//   * each warp then walks the chunk's non-empty channels (ascending) and, per channel,
-//     its nonzero positions (ascending): one jump-table branch on the position selects
-//     a block of <= 9 FMAs with compile-time accumulator and weight registers
-//     (si3x3_cases.inc).  The next channel's 9 weights are fetched while the current
-//     channel is applied.
+//   * a warp owns a 4 x 8 output tile of one image and 32*KT filters (lane = filter;
+//     KT = 2 from K = 128 up: the accumulator of an output is the register pair of two
+//     filters and every FMA an FFMA2 with the input value broadcast); a CTA's NW warps
+//     cover up to 512 filters of the same tile.
+//   * per 32-channel chunk the CTA decodes the 6 x 10 input region's node fibers into
+//     shared memory: values [32][region] plus, per channel, a bitmap of the region
+//     positions holding a node (each fiber read as one coalesced 32-node warp load,
+//     cursors kept across chunks; 8-warp CTAs prefetch the next chunk's windows with
+//     cp.async), then compacts the bitmaps into per-channel entry lists {pos, value}.
+//   * each warp walks the chunk's live channels (ascending) and, per channel, its
+//     entries (positions ascending): one jump-table branch per entry selects a block of
+//     <= 9 FMAs with compile-time accumulator and weight registers (si3x3_cases.inc).
+//     The next channel's weights are fetched while the current channel is applied.
 // No global atomics; the summation order is fixed, so results are deterministic and
-// independent of the launch configuration for a given tile size.
+// independent of the batch, KT and the CTA size.
 #include <algorithm>
 #include <stdlib.h>
 
