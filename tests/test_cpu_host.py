@@ -57,6 +57,24 @@ def test_abi_rejects_bad_arguments_without_gpu():
                   0, 4, None)
     with pytest.raises(_lib.FscnnError, match="row pitch"):
         _lib.call("fscnn_whc_to_nchw_ex", None, 1, 1, 4, 8, None, 8, 1, None)
+    # the channel-major sparse-input entries
+    with pytest.raises(_lib.FscnnError, match="bad SI pack"):
+        _lib.call("fscnn_si_pack_fast", None, 0, 4, None, None)
+    with pytest.raises(_lib.FscnnError, match="bad extents"):
+        _lib.call("fscnn_si_conv3x3_fast", None, None, 0, 1, 0, 4, 4, None, 8, None, None, None)
+    with pytest.raises(_lib.FscnnError, match="null buffer"):
+        _lib.call("fscnn_si_conv3x3_fast", None, None, 4, 1, 2, 4, 4, None, 8, None, None, None)
+    with pytest.raises(_lib.FscnnError, match="too large"):
+        _lib.call("fscnn_si_conv3x3_fast", 8, 8, 4, 70000, 2, 4, 4, 8, 8, None, 8, None)
+    lib = _lib.load()
+    assert lib.fscnn_si_fast_bank_floats(0, 4) == 0
+    # K padded to whole CTAs: 40 filters -> 1 per lane, 2 warps of 32 = 64
+    assert lib.fscnn_si_fast_bank_floats(40, 3) == 3 * 9 * 64
+    # 512 filters -> 2 per lane, 8 warps = 512
+    assert lib.fscnn_si_fast_bank_floats(512, 2) == 2 * 9 * 512
+    # the sparse-filter kernel accepts 1, 2, 4 and 8 filters per warp, not 3
+    with pytest.raises(_lib.FscnnError, match="kt must be"):
+        _lib.call("fscnn_sf_pack_offsets", 8, 4, 4, 3, 8, 8, None, 0, None)  # dummy non-null pointers
 
 
 def test_no_cpu_fallback():
