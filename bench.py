@@ -185,6 +185,19 @@ def run_reference(args):
     return 0
 
 
+def _relaunch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-run this command under
+    torch.distributed.run with N local ranks (one process per GPU, 127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -196,6 +209,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -209,10 +224,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FSCNN_DIST_BACKEND=gloo: functional check of the N-rank path on a box with fewer
+    # GPUs than ranks (ranks share GPUs, collectives through host memory) -- not a
+    # performance configuration; the default is NCCL with one GPU per rank
+    backend = os.environ.get("FSCNN_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     per_gpu, zf, desc = WORKLOADS[args.workload]
     if args.workload == "c5":
@@ -224,31 +248,30 @@ def main():
     layers = wl.vgg16_weights(seed=103, zero_frac=zf) if rank == 0 else None
 
     # filters: rank 0 encodes (reference node format), NCCL broadcast, every rank packs
+    # (distributed.ShardedVGG); one GPU: the engine directly
+    sharded = None
     if world > 1:
-        if rank == 0:
-            eng0 = VGGEngine(layers, batch=n_local, hw=hw)
-            banks = [(s.nodes[: s.n_nodes], s.seg_off, s.tensor_off, s.matrix_off, s.bias) for s in eng0.steps]
-        else:
-            banks = None
-        got = pdist.broadcast_banks(banks, dev)
-        enc = []
-        for nodes, seg, ten, mat, bias in got:
-            k = int(ten.numel())
-            enc.append((nodes, int(nodes.shape[0]), seg, ten, mat, bias.cpu().numpy(), k))
-        eng = eng0 if rank == 0 else VGGEngine(None, batch=n_local, hw=hw, encoded=enc)
+        sharded = pdist.ShardedVGG(layers, hw=hw, device=dev)
+        eng = sharded.engine
     else:
         eng = VGGEngine(layers, batch=n_local, hw=hw)
+    n_total = n_local * world if args.workload == "c3" else per_gpu
 
     # inputs resident in HBM (per rank seeded shard)
-    x_np = wl.vgg16_input(n_local, seed=104 + rank)
+    def shard_input(r):
+        if args.workload == "c3":
+            return wl.vgg16_input(n_local, seed=104 + r)
+        a, b = pdist.shard_range(per_gpu, r, world)
+        return wl.vgg16_input(per_gpu, seed=104)[a:b]
+
+    x_np = shard_input(rank)
     x = torch.from_numpy(x_np).to(dev)
     flops_img = eng.flops_per_image()
 
     def step():
-        y = eng.forward_device(x)
-        if world > 1:
-            pdist.gather_outputs(y.contiguous())
-        return y
+        if sharded is not None:
+            return sharded.forward_device(x, total=n_total)
+        return eng.forward_device(x)
 
     for _ in range(args.warmup):
         step()
@@ -274,7 +297,7 @@ def main():
     sampler.stop()
     if world > 1:
         elapsed_ms = pdist.max_over_ranks(elapsed_ms, dev)
-    images = n_local * world * args.steps
+    images = n_total * args.steps
     value = images / (elapsed_ms * 1e-3)
 
     # per-layer kernel times on the launching stream (roofline of the dominant kernel)
@@ -310,7 +333,30 @@ def main():
 
     # e2e through the public API (host DenseTensor3 in, host DenseTensor3 out)
     e2e = None
-    if rank == 0:
+    if world > 1:
+        # every rank runs ShardedVGG.forward on the full host batch concurrently (its shard
+        # H2D, its stack, NCCL all-gather of the device outputs, D2H of the full batch on
+        # rank 0); the time is the max over ranks of each rank's wall clock
+        full_np = np.concatenate([shard_input(r) for r in range(world)]) if args.workload == "c3" \
+            else wl.vgg16_input(per_gpu, seed=104)
+        batch = network.pinned_batch(n_total, (3, hw, hw))
+        lo, hi = sharded.shard(n_total)
+        for i in range(lo, hi):
+            batch[i].data[:] = DenseTensor3.from_array(full_np[i]).data
+        e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+        for _ in range(3):
+            sharded.forward(batch, dst=0)
+        torch.cuda.synchronize()
+        passes = sorted(sharded.timed_forward(batch, dst=0, reps=e2e_steps)[1] for _ in range(3))
+        dt = passes[1]
+        e2e = {"value": n_total * e2e_steps / dt, "unit": "images/s",
+               "h2d_bytes_per_step": int(n_total * 3 * hw * hw * 4),
+               "d2h_bytes_per_step": int(n_total * eng.out_c * eng.out_hw * eng.out_hw * 4),
+               "path": f"distributed.ShardedVGG.forward(list[DenseTensor3]) on {world} ranks concurrently: "
+                       "each rank's shard H2D from pinned host memory, its stack, NCCL all-gather of the "
+                       "device outputs, D2H of the full batch on rank 0; max over ranks of the wall clock, "
+                       "median of 3 timed passes"}
+    elif rank == 0:
         prepared = network.prepared_from_engine(eng)
         # the step's inputs sit in pinned host memory (network.pinned_batch: one DMA, no
         # host packing); pageable DenseTensor3 lists are packed first (e2e["pageable"])
@@ -345,9 +391,6 @@ def main():
                        "3 timed passes",
                "pageable": {"value": n_local * e2e_steps / dt_pageable,
                             "note": "same call with pageable numpy inputs (threaded pack into pinned staging)"}}
-        if world > 1:
-            e2e["value"] *= world  # every rank runs its shard concurrently; rank 0's rate x N
-            e2e["note"] = "rank-0 public-API rate x world size"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -361,11 +404,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.workload == "c3" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded numpy, workloads.py): x~N(0,1), W~N(0,sqrt(2/fan_in)) i.i.d. masked",
-            "config": {"workload": desc, "global_batch": n_local * world, "seq_len": None,
+            "config": {"workload": desc, "global_batch": n_total, "seq_len": None,
                        "parallelism": f"dp{world} (batch-sharded, filters broadcast once)",
+                       "collectives": backend if world > 1 else None,
                        "filter_zero_fraction": zf,
                        "l2": "working set > L2 (activations 0.4 GB per layer at batch 32)"},
-            "nnz_gflops": flops_img * n_local * world * args.steps / (elapsed_ms * 1e-3) / 1e9,
+            "nnz_gflops": flops_img * n_total * args.steps / (elapsed_ms * 1e-3) / 1e9,
             "nnz_gflop_per_image": flops_img / 1e9,
             "roofline": {"bound": "fp32", "kernel": "sf3x3_kernel: the 13 convs, each timed as one full-batch launch on its stream (the step runs them as two half-batch streams)",
                          "achieved": achieved_tf, "peak": peak_meas, "unit": "TFLOP/s",

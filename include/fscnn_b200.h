@@ -256,6 +256,12 @@ int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int
 
 /* FP32 CUDA-core throughput probe (roofline denominator): `blocks` x 256 threads,
  * each 8 independent FFMA chains of 16*iters steps = 256*blocks*iters*256 FLOPs. */
+/* Row-pitched copy of `rows` rows of w floats: y[r*ldy + coly + j] = x[r*ldx + colx + j].
+ * Dense NCHW <-> the halo-column activation layout (no reference counterpart: staging
+ * around the conv stack of network.py:410-534). */
+int fscnn_pitch_copy(const float *x, int64_t rows, int w, int ldx, int colx, float *y, int ldy,
+                     int coly, void *stream);
+
 int fscnn_fp32_probe(float *out, int blocks, int iters, void *stream);
 
 #ifdef __cplusplus

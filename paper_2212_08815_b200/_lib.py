@@ -60,6 +60,7 @@ _SIGNATURES = {
     "fscnn_nchw_to_whc": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_whc_to_nchw_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
     "fscnn_nchw_to_whc_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fscnn_pitch_copy": (_i32, [_vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
     "fscnn_fp32_probe": (_i32, [_vp, _i32, _i32, _vp]),
 }
 

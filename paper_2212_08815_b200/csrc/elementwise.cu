@@ -273,6 +273,22 @@ inline unsigned grid_for(int64_t n, int threads) {
     return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
 }
 
+// Row-pitched copy: rows of w floats from x (pitch ldx, first column colx) to y (pitch
+// ldy, first column coly) -- dense NCHW <-> the halo-column activation layout.  One warp
+// per row segment of 32 floats.
+__global__ void pitch_copy_kernel(const float *__restrict__ x, int64_t rows, int w, int ldx, int colx,
+                                  float *__restrict__ y, int ldy, int coly) {
+    const int segs = (w + 31) >> 5;
+    const int64_t total = rows * segs;
+    const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += stride) {
+        const int64_t r = t / segs;
+        const int col = (int)(t % segs) * 32 + lane;
+        if (col < w) y[r * ldy + coly + col] = x[r * ldx + colx + col];
+    }
+}
+
 }  // namespace
 }  // namespace fscnn
 
@@ -405,6 +421,20 @@ int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w
     kcrs_to_crsk_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(w_kcrs, k, c * r * s,
                                                                             w_crsk);
     FSCNN_LAUNCH_CHECK("kcrs_to_crsk_kernel");
+    return FSCNN_OK;
+}
+
+int fscnn_pitch_copy(const float *x, int64_t rows, int w, int ldx, int colx, float *y, int ldy,
+                     int coly, void *stream) {
+    FSCNN_REQUIRE(rows >= 0 && w >= 0 && colx >= 0 && coly >= 0, "negative extent");
+    FSCNN_REQUIRE(ldx >= w + colx && ldy >= w + coly, "row pitch too small");
+    if (rows == 0 || w == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && y, "null buffer");
+    const int64_t warps = rows * ((w + 31) / 32);
+    const int64_t blocks = (warps + 7) / 8;
+    pitch_copy_kernel<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, as_stream(stream)>>>(
+        x, rows, w, ldx, colx, y, ldy, coly);
+    FSCNN_LAUNCH_CHECK("pitch_copy_kernel");
     return FSCNN_OK;
 }
 

@@ -300,6 +300,29 @@ def to_halo(x: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def pitch_copy(x: torch.Tensor, rows: int, w: int, ldx: int, colx: int, y: torch.Tensor, ldy: int,
+               coly: int) -> torch.Tensor:
+    call("fscnn_pitch_copy", ptr(x), rows, w, ldx, colx, ptr(y), ldy, coly, stream())
+    return y
+
+
+def nchw_into_halo(x: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """Dense [N, C, H, W] into a halo-column buffer [N, C, H, pitch] (one kernel)."""
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    assert out.is_contiguous() and tuple(out.shape[:3]) == (n, c, h) and out.shape[3] >= w + 1
+    return pitch_copy(x, n * c * h, w, w, 0, out, int(out.shape[3]), 1)
+
+
+def halo_to_nchw(xh: torch.Tensor, w: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Logical [N, C, H, w] of a halo-column buffer -> dense contiguous [N, C, H, w]."""
+    assert xh.is_contiguous()
+    n, c, h, ld = (int(v) for v in xh.shape)
+    if out is None:
+        out = torch.empty((n, c, h, w), dtype=torch.float32, device=xh.device)
+    return pitch_copy(xh, n * c * h, w, ld, 1, out, w, 0)
+
+
 def from_halo(xh: torch.Tensor, w: int) -> torch.Tensor:
     """View of the logical [N, C, H, W] data inside a halo-column buffer."""
     return xh[..., 1 : w + 1]

@@ -121,8 +121,7 @@ class VGGEngine:
     def stage_input(self, x: torch.Tensor) -> torch.Tensor:
         """Copy a dense [N, C, H, W] CUDA batch into the engine's halo input buffer."""
         self._buffers(int(x.shape[0]))
-        self._in[..., 1 : self.hw + 1].copy_(x)
-        return self._in
+        return device.nchw_into_halo(x, self._in)
 
     def run(self, xh: torch.Tensor, parts: int = 2) -> torch.Tensor:
         """Run the stack on a halo-layout input; returns the halo output buffer.
@@ -210,11 +209,38 @@ class VGGEngine:
                               out=bufs[0][lo:hi], w=self.hw, ly=first.ly, cta_warps=warps)
         return device.halo_to_whc(self._run_from(1, bufs[0]), self.out_hw)
 
+    def run_exact(self, x: torch.Tensor) -> torch.Tensor:
+        """Dense [N, C, H, W] -> [N, C', H', W'] through the reference-order kernels:
+        per conv the bit-exact sparse-filter kernel (taps kw outer, kh inner, channels
+        ascending; layers.py:170-180) with bias and ReLU, then the standalone 2x2
+        max-pool (layers.py:250-271) -- what set_exact(True) asks of the stack."""
+        cur = x.contiguous()
+        for st in self.steps:
+            cur = device.sf_conv_exact(cur, st.nodes, st.seg_off, st.k, 3, 3, 1, 1, st.bias, relu=True)
+            if st.pool:
+                cur = device.pool2d(cur, 2, 2, True)
+        return cur
+
+    def forward_from_host_exact(self, h_src: torch.Tensor, n: int, fill=None) -> torch.Tensor:
+        """forward_from_host through run_exact: pinned (W,H,C) images -> device (W,H,C)."""
+        elems = self.in_c * self.hw * self.hw
+        if fill is not None:
+            fill(0, n)
+        d = h_src[: n * elems].to(self.steps[0].bias.device, non_blocking=True)
+        x = device.whc_to_nchw(d, n, self.in_c, self.hw, self.hw)
+        return device.nchw_to_whc(self.run_exact(x))
+
     def forward_device(self, x: torch.Tensor) -> torch.Tensor:
-        """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer)."""
+        """x: CUDA [N, C, H, W] -> [N, 512, H/32, W/32] (a view into the output buffer;
+        ``contiguous=True``: a dense copy, made by the library's pitch-copy kernel)."""
         assert x.shape[1] == self.in_c and x.shape[2] == self.hw and x.shape[3] == self.hw
         y = self.run(self.stage_input(x))
         return device.from_halo(y, self.out_hw)
+
+    def forward_device_dense(self, x: torch.Tensor) -> torch.Tensor:
+        """forward_device with a dense contiguous [N, 512, H/32, W/32] result."""
+        y = self.run(self.stage_input(x))
+        return device.halo_to_nchw(y, self.out_hw)
 
     def flops_per_image(self) -> int:
         """Exact nnz-FLOPs per image: 2 x in-bounds multiplies (kernels.py:108-133)."""

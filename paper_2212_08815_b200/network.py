@@ -353,15 +353,14 @@ def pinned_batch(n: int, dims) -> list:
     return [DenseTensor3((c, h, w), arr[i]) for i in range(n)]
 
 
-def _forward_engine(prepared: PreparedNet, batch) -> list:
-    import torch
-
+def _engine_device_forward(prepared: PreparedNet, batch):
+    """Host DenseTensor3 batch -> the engine's device (W,H,C) output [n, W', H', C']
+    (pinned H2D in parts overlapped with the first conv; the caller holds _engine_lock)."""
     eng = prepared.engine
     n = len(batch)
     c, h, w = prepared.net.input_dims
-    oc, ohw = eng.out_c, eng.out_hw
     elems = c * h * w
-    h_in, _ = _staging.get(n, elems, oc * ohw * ohw)
+    h_in, _ = _staging.get(n, elems, eng.out_c * eng.out_hw * eng.out_hw)
     src = _staging.pinned_source(batch, elems)
     fill = None
     if src is None:  # pageable inputs: pack each half into pinned staging just before its copy
@@ -372,14 +371,27 @@ def _forward_engine(prepared: PreparedNet, batch) -> list:
                 np_in[i] = batch[i].data
 
         src = h_in
-    whc = eng.forward_from_host(src, n, fill)
-    # outputs go straight into a fresh pinned buffer (torch's caching host allocator
-    # recycles it once the returned arrays are gone), no host-side copy
+    if ly._EXACT:  # set_exact(True): the reference-order kernels, bit-exact
+        return eng.forward_from_host_exact(src, n, fill)
+    return eng.forward_from_host(src, n, fill)
+
+
+def _whc_to_host(whc, n: int, oc: int, ohw: int) -> list:
+    """Device (W,H,C) outputs -> host DenseTensor3 list (one D2H into fresh pinned memory;
+    torch's caching host allocator recycles it once the returned arrays are gone)."""
+    import torch
+
     res = torch.empty(n * oc * ohw * ohw, dtype=torch.float32, pin_memory=True)
-    res.copy_(whc.view(-1), non_blocking=True)
+    res.copy_(whc.reshape(-1), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     out = res.numpy().reshape(n, -1)
     return [DenseTensor3((oc, ohw, ohw), out[i]) for i in range(n)]
+
+
+def _forward_engine(prepared: PreparedNet, batch) -> list:
+    eng = prepared.engine
+    whc = _engine_device_forward(prepared, batch)
+    return _whc_to_host(whc, len(batch), eng.out_c, eng.out_hw)
 
 
 _BATCHED = True  # tests switch it off to compare against the per-image layer path

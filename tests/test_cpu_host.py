@@ -207,7 +207,10 @@ def _dist_worker(rank, world, port, q):
         y = torch.full((2, 3), float(rank))
         gathered = [g.numpy().tolist() for g in pd.gather_outputs(y)]
         mx = pd.max_over_ranks(float(rank + 1), dev)
-        q.put((rank, sig, (lo, hi), gathered, mx))
+        # unequal shards (5 items over 2 ranks: 3 + 2) gathered in rank order
+        a, b = pd.shard_range(5, rank, world)
+        full = pd.gather_batch(torch.arange(a, b, dtype=torch.float32).repeat_interleave(4).view(b - a, 2, 2), 5)
+        q.put((rank, sig, (lo, hi), gathered, mx, full.numpy().tolist(), str(pd.comm_device(dev))))
     finally:
         dist.destroy_process_group()
 
@@ -233,6 +236,9 @@ def test_batch_sharded_driver_gloo_world2():
     assert res[0][1] == (0, 5) and res[1][1] == (5, 10)
     assert res[0][2] == [[[0.0] * 3] * 2, [[1.0] * 3] * 2]  # rank-ordered gather
     assert res[0][3] == res[1][3] == 2.0
+    want = [[[float(i)] * 2] * 2 for i in range(5)]
+    assert res[0][4] == res[1][4] == want
+    assert res[0][5] == "cpu"
 
 
 def test_shard_range_covers_batch():

@@ -225,6 +225,30 @@ def test_vgg_stack_forward_matches_reference():
     assert normwise_err(got2, g["y"]) <= TOL
 
 
+def test_vgg_engine_honours_set_exact_bitwise():
+    """set_exact(True) routes the fused VGG engine (forward without record_density)
+    through the reference-order kernels: bit-exact with the reference's own output
+    (network.py:410-428 over layers.py:302-323)."""
+    g, net, weights = _small_vgg()
+    prepared = fs.prepare(net, weights)
+    batch = [fs.DenseTensor3.from_array(a) for a in g["x"]]
+    fs.set_exact(True)
+    try:
+        res = fs.forward(prepared, batch)
+        got = np.stack([o.to_array() for o in res.outputs])
+        assert got.tobytes() == np.ascontiguousarray(g["y"], np.float32).tobytes()
+        # same through a pinned batch (the zero-copy source)
+        pinned = fs.pinned_batch(len(batch), (3, 32, 32))
+        for t, src in zip(pinned, batch):
+            t.data[:] = src.data
+        got_p = np.stack([o.to_array() for o in fs.forward(prepared, pinned).outputs])
+        assert got_p.tobytes() == got.tobytes()
+    finally:
+        fs.set_exact(False)
+    fast = np.stack([o.to_array() for o in fs.forward(prepared, batch).outputs])
+    assert normwise_err(fast, g["y"]) <= TOL
+
+
 def test_worker_strategy_and_batch_invariance_bitwise():
     g, net, weights = _small_vgg()
     prepared = fs.prepare(net, weights)
@@ -317,3 +341,66 @@ def test_full_size_config5_batch_invariance(oracle):
         banks.append((nodes, seg, wt.shape[0], b))
     ref = oracle.vgg_forward(x[:1].cpu().numpy(), banks)
     assert normwise_err(y[:1].cpu().numpy(), ref) <= TOL
+
+
+# -- batch-sharded multi-process stack (distributed.ShardedVGG) ----------------------
+
+
+def _sharded_worker(rank, world, port, layers, xs, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2212_08815_b200 import distributed as pd
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)  # both ranks share the one GPU: gloo carries the collectives
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sh = pd.ShardedVGG(layers if rank == 0 else None, hw=32, device=torch.device("cuda", 0))
+        outs, secs = sh.timed_forward([fs.DenseTensor3.from_array(a) for a in xs])
+        lo, hi = sh.shard(len(xs))
+        x_local = torch.from_numpy(np.stack(xs[lo:hi])).cuda()
+        full = sh.forward_device(x_local, total=len(xs)).cpu().numpy()
+        q.put((rank, [o.data.tobytes() for o in outs], full.tobytes(), secs > 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_forward_byte_identical_world2():
+    """SPMD batch-sharded forward over two ranks (gloo; both on cuda:0) returns, on every
+    rank, exactly the single-GPU outputs -- the north star's 'outputs byte-identical at
+    1/2/4/8 GPUs' (reference worker invariance, pkg/tests/test_acceptance.py:311-351).
+    Five images: unequal shards (3 + 2)."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2212_08815_b200.engine import VGGEngine
+
+    layers = wl.vgg16_weights(seed=21, zero_frac=0.95, scale=0.125)
+    rng = np.random.default_rng(22)
+    xs = [rng.standard_normal((3, 32, 32)).astype(np.float32) for _ in range(5)]
+    eng = VGGEngine(layers, batch=5, hw=32)
+    prepared = nw.prepared_from_engine(eng)
+    ref = [o.data.tobytes() for o in fs.forward(prepared, [fs.DenseTensor3.from_array(a) for a in xs]).outputs]
+    ref_dev = eng.forward_device(torch.from_numpy(np.stack(xs)).cuda()).contiguous().cpu().numpy().tobytes()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, layers, xs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        outs, full, timed = res[r]
+        assert outs == ref, r
+        assert full == ref_dev, r
+        assert timed
