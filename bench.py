@@ -255,6 +255,10 @@ def main():
         eng = sharded.engine
     else:
         eng = VGGEngine(layers, batch=n_local, hw=hw)
+    t_jit = time.perf_counter()
+    eng.wait_compiled()  # the specialised kernels' compile jobs (cached on disk by content hash)
+    t_jit = time.perf_counter() - t_jit
+    jit_on = all(st.jit is not None for st in eng.steps)
     n_total = n_local * world if args.workload == "c3" else per_gpu
 
     # inputs resident in HBM (per rank seeded shard)
@@ -312,22 +316,22 @@ def main():
         for i, (st, out) in enumerate(zip(eng.steps, bufs)):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            bank, warps = st.plan_for(n_local)
-            pdev.sf_conv3x3(cur, bank, st.bias, relu=True, pool=st.pool, out=out, w=w, ly=st.ly, cta_warps=warps)
+            st.conv(cur, out, w, n_local)
             b.record()
             b.synchronize()
             layer_ms[i] += a.elapsed_time(b) / reps
             cur = out
             w = w // 2 if st.pool else w
     peak_meas, peak_nom = fp32_peak_tflops(torch, _lib)
-    # DRAM traffic per launch of the dominant kernel, from the committed ncu launch list
-    # of this same command (profiles/r01_bench_launches_summary.json), when present
+    # DRAM traffic per layer of the dominant kernel, from the committed ncu summary of this
+    # same command (profiles/r02_bench_traffic.json), when present
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r01_bench_launches_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r02_bench_traffic.json" if jit_on else "r01_bench_launches_summary.json")
     if os.path.exists(prof) and args.workload == "c3":
         with open(prof) as fh:
-            traffic = json.load(fh).get("sf3x3_dram_bytes_per_launch")
-        traffic_src = "profiles/r01_bench_launches_summary.json (ncu launch list, cold cache)"
+            d = json.load(fh)
+        traffic = d.get("dram_bytes_per_layer", d.get("sf3x3_dram_bytes_per_launch"))
+        traffic_src = f"profiles/{os.path.basename(prof)} (ncu, cold cache)"
     kern_ms = sum(layer_ms)
     achieved_tf = flops_img * n_local / (kern_ms * 1e-3) / 1e12
 
@@ -411,7 +415,11 @@ def main():
                        "l2": "working set > L2 (activations 0.4 GB per layer at batch 32)"},
             "nnz_gflops": flops_img * n_total * args.steps / (elapsed_ms * 1e-3) / 1e9,
             "nnz_gflop_per_image": flops_img / 1e9,
-            "roofline": {"bound": "fp32", "kernel": "sf3x3_kernel: the 13 convs, each timed as one full-batch launch on its stream (the step runs them as two half-batch streams)",
+            "roofline": {"bound": "fp32",
+                         "kernel": ("sfjit: per-layer specialised sparse-filter kernels (one per 32-filter group, "
+                                    "weights as FFMA2 immediates), the 13 convs each timed as one full-batch layer "
+                                    "launch on its stream" if jit_on else
+                                    "sf3x3_kernel: the 13 convs, each timed as one full-batch launch on its stream"),
                          "achieved": achieved_tf, "peak": peak_meas, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_meas,
                          "peak_source": "measured FFMA probe (fscnn_fp32_probe) on this GPU; "
@@ -423,6 +431,9 @@ def main():
                          "algorithmic_bytes_per_launch": eng.bytes_per_image() * n_local / len(eng.steps),
                          "per_layer_ms": [round(v, 4) for v in layer_ms]},
             "gpu_launches": launches,
+            "prepare": {"sfjit": jit_on, "compile_wait_s": round(t_jit, 2),
+                        "note": "bank compile (nvJitLink on host threads, overlapped with encoding) joined "
+                                "before the timed region; cached on disk by content hash"},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -256,6 +256,33 @@ int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int
 
 /* FP32 CUDA-core throughput probe (roofline denominator): `blocks` x 256 threads,
  * each 8 independent FFMA chains of 16*iters steps = 256*blocks*iters*256 FLOPs. */
+/* Per-layer specialised sparse-filter 3x3/s1/p1 conv (+bias, ReLU, fused 2x2 max-pool):
+ * the bank's nonzero pattern and values are compiled into the kernel (one straight-line
+ * kernel per group of up to 32 filters, weights as FFMA2 immediates; PTX generated here,
+ * compiled with nvJitLink on host threads, cached on disk by content hash).  Replaces
+ * the same reference routine as fscnn_sf_conv3x3_ex -- _conv_all_filters_kernel
+ * (layers.py:170-180) over _window_acc (kernels.py:78-97) -- with the same accumulation
+ * order, so its outputs are bit-identical to fscnn_sf_conv3x3_ex's.
+ *   create: w_kc33 = dense host bank [k][c][3][3] (+-0.0 entries are absent nodes),
+ *           bias = host [k] or NULL; h, w even; flags: bits 0-7 filters per group
+ *           (0 = 32), bits 8-15 warps per CTA (0 = 12).  Returns immediately: the
+ *           compile runs in the background; wait (or the first launch) joins it.
+ *   launch: x = halo-column input [n][c][h][ldi] (logical column j at memory column j+1,
+ *           column 0 zero, ldi >= w+1 and a multiple of 4, 16-byte aligned);
+ *           y = halo-column output [n][k][h'][ldo] (h' = h/2, w' = w/2 with the pool;
+ *           columns 0 and > w' of y are not written). */
+typedef struct fscnn_sfjit fscnn_sfjit;
+int fscnn_sfjit_create(const float *w_kc33, const float *bias, int k, int c, int h, int w, int relu,
+                       int pool, int flags, fscnn_sfjit **out);
+int fscnn_sfjit_compiled(fscnn_sfjit *j); /* join the compile jobs (no GPU needed) */
+int fscnn_sfjit_wait(fscnn_sfjit *j);     /* compiled + modules loaded in the current context */
+int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y, int ldo, void *stream);
+int fscnn_sfjit_info(fscnn_sfjit *j, int64_t *info, double *secs);
+void fscnn_sfjit_destroy(fscnn_sfjit *j);
+/* PTX of one group (inspection, CPU tests): length, copied into buf when cap > length. */
+int64_t fscnn_sfjit_ptx(const float *w_kc33, const float *bias, int k, int c, int h, int w, int relu,
+                        int pool, int flags, int group, char *buf, int64_t cap);
+
 /* Row-pitched copy of `rows` rows of w floats: y[r*ldy + coly + j] = x[r*ldx + colx + j].
  * Dense NCHW <-> the halo-column activation layout (no reference counterpart: staging
  * around the conv stack of network.py:410-534). */

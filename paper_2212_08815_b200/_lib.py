@@ -60,6 +60,13 @@ _SIGNATURES = {
     "fscnn_nchw_to_whc": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "fscnn_whc_to_nchw_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
     "fscnn_nchw_to_whc_ex": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fscnn_sfjit_create": (_i32, [_vp, _vp] + [_i32] * 7 + [_vp]),
+    "fscnn_sfjit_compiled": (_i32, [_vp]),
+    "fscnn_sfjit_wait": (_i32, [_vp]),
+    "fscnn_sfjit_ptx": (_i64, [_vp, _vp] + [_i32] * 8 + [_vp, _i64]),
+    "fscnn_sfjit_launch": (_i32, [_vp, _vp, _i32, _i32, _vp, _i32, _vp]),
+    "fscnn_sfjit_info": (_i32, [_vp, _vp, _vp]),
+    "fscnn_sfjit_destroy": (None, [_vp]),
     "fscnn_pitch_copy": (_i32, [_vp, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
     "fscnn_fp32_probe": (_i32, [_vp, _i32, _i32, _vp]),
 }

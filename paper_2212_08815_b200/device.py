@@ -355,6 +355,69 @@ def sf_conv3x3(x: torch.Tensor, bank: PackedBank, bias: torch.Tensor | None, rel
     return out
 
 
+def sfjit_enabled() -> bool:
+    """The VGG engine compiles each bank into specialised kernels unless FSCNN_SFJIT=0."""
+    return os.environ.get("FSCNN_SFJIT", "1") != "0"
+
+
+class SfJit:
+    """Per-layer specialised sparse-filter conv (fscnn_sfjit_*): the filter bank is
+    compiled into straight-line kernels (one per group of 32 filters).  Bit-identical to
+    sf_conv3x3 on the same bank (same accumulation order).  Construction submits the
+    compile jobs and returns; the first call (or wait()) joins them."""
+
+    INFO = ("groups", "ctas_per_image_or_minus_images_per_cta", "warps", "filters_per_group", "channels_per_chunk", "stages",
+            "smem_bytes", "box_rows", "row_pitch", "boxes_per_cta", "registers", "cached_groups")
+
+    def __init__(self, w_kc33, bias, h: int, w: int, relu: bool = True, pool: bool = False, flags: int = 0):
+        import ctypes
+
+        wt = np.ascontiguousarray(w_kc33.detach().cpu().numpy() if torch.is_tensor(w_kc33) else w_kc33,
+                                  dtype=np.float32)
+        self.k, self.c = int(wt.shape[0]), int(wt.shape[1])
+        assert wt.shape[2:] == (3, 3)
+        b = None
+        if bias is not None:
+            b = np.ascontiguousarray(bias.detach().cpu().numpy() if torch.is_tensor(bias) else bias, dtype=np.float32)
+        self.h, self.w, self.relu, self.pool = h, w, bool(relu), bool(pool)
+        handle = ctypes.c_void_p()
+        call("fscnn_sfjit_create", wt.ctypes.data, b.ctypes.data if b is not None else None, self.k, self.c, h, w,
+             int(relu), int(pool), int(flags), ctypes.byref(handle))
+        self._h = handle
+        self._lib = _lib.load()
+
+    def wait(self) -> "SfJit":
+        call("fscnn_sfjit_wait", self._h)
+        return self
+
+    def info(self) -> dict:
+        import ctypes
+
+        v = (ctypes.c_int64 * 12)()
+        sec = (ctypes.c_double * 2)()
+        call("fscnn_sfjit_info", self._h, v, sec)
+        d = dict(zip(self.INFO, list(v)))
+        d["compile_seconds_total"] = sec[1]
+        return d
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, n: int | None = None) -> torch.Tensor:
+        """x: halo-column buffer [N, C, H, pitch] -> halo-column output [N, K, H', pitch']."""
+        n = int(x.shape[0]) if n is None else n
+        assert int(x.shape[1]) == self.c and int(x.shape[2]) == self.h and x.stride(3) == 1
+        ldi = int(x.stride(2))
+        ho, wo = (self.h // 2, self.w // 2) if self.pool else (self.h, self.w)
+        if out is None:
+            out = halo_empty(n, self.k, ho, wo, x.device)
+        call("fscnn_sfjit_launch", self._h, ptr(x), n, ldi, ptr(out), int(out.stride(2)), stream())
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and getattr(self, "_lib", None) is not None:
+            self._lib.fscnn_sfjit_destroy(h)
+            self._h = None
+
+
 def sf_conv_exact(x: torch.Tensor, nodes: torch.Tensor, seg_off: torch.Tensor, k: int, h_f: int,
                   w_f: int, stride_: int, pad: int, bias: torch.Tensor | None, relu: bool = False,
                   out: torch.Tensor | None = None) -> torch.Tensor:

@@ -17,6 +17,7 @@ banks (see distributed.py) and shard the batch.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -42,6 +43,16 @@ class ConvStep:
     n_nodes: int
     ly: int = 0
     small: dict | None = None  # kt -> packed stream with 1 / 2 filters per warp (small grids)
+    jit: device.SfJit | None = None  # the bank compiled into per-group kernels (sfjit.cu)
+
+    def conv(self, x: torch.Tensor, out: torch.Tensor, w: int, n_plan: int) -> torch.Tensor:
+        """conv3x3 + bias + ReLU [+ 2x2 max-pool] of a halo-column batch into ``out``:
+        the specialised kernels when compiled, else the jump-table kernel (identical bits)."""
+        if self.jit is not None:
+            return self.jit(x, out=out)
+        bank, warps = self.plan_for(n_plan)
+        return device.sf_conv3x3(x, bank, self.bias, relu=True, pool=self.pool, out=out, w=w, ly=self.ly,
+                                 cta_warps=warps)
 
     def plan_for(self, n: int) -> tuple[device.PackedBank, int]:
         """(packed stream, warps per CTA) for a launch over n images: fewer filters per
@@ -65,9 +76,11 @@ class VGGEngine:
     """
 
     def __init__(self, layers, batch: int, hw: int = 224, plan=VGG16_PLAN, in_c: int = 3,
-                 encoded=None):
+                 encoded=None, jit: bool | None = None):
         self.batch, self.hw, self.plan = batch, hw, list(plan)
         self.in_c = in_c
+        if jit is None:
+            jit = device.sfjit_enabled()
         dev = torch.device("cuda", torch.cuda.current_device())
         self.steps: list[ConvStep] = []
         c, h = in_c, hw
@@ -92,13 +105,20 @@ class VGGEngine:
                 bias_t = bias_t.to(dev, torch.float32).contiguous()
             bank = device.sf_pack(dense)
             small = {kt: device.sf_pack(dense, kt) for kt in (1, 2)} if bank.kt == 4 else None
-            self.steps.append(ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes,
-                                       device.pick_ly(c, h), small))
+            step = ConvStep(k, c, h, h, pool, bank, bias_t, nodes, seg, ten, mat, n_nodes, device.pick_ly(c, h), small)
+            if jit and h % 2 == 0:
+                # compile jobs are submitted here and run on host threads while the next
+                # banks are encoded; the first forward joins them
+                step.jit = device.SfJit(dense, bias_t, h, h, relu=True, pool=pool)
+            self.steps.append(step)
             c = k
             if pool:
                 h //= 2
             li += 1
         self.out_c, self.out_hw = c, h
+        # batch split over streams: helps the jump-table kernel's partial last waves; the
+        # specialised kernels already spread each layer over concurrent per-group launches
+        self.parts = 1 if all(st.jit is not None for st in self.steps) else 2
         self._bufs = None
         self._bufs_batch = None
 
@@ -123,7 +143,7 @@ class VGGEngine:
         self._buffers(int(x.shape[0]))
         return device.nchw_into_halo(x, self._in)
 
-    def run(self, xh: torch.Tensor, parts: int = 2) -> torch.Tensor:
+    def run(self, xh: torch.Tensor, parts: int | None = None) -> torch.Tensor:
         """Run the stack on a halo-layout input; returns the halo output buffer.
 
         The batch is split over ``parts`` streams, each walking all layers on its slice:
@@ -132,7 +152,14 @@ class VGGEngine:
         stack at batch 32).  Results are identical (the kernels are batch-position
         invariant).
         """
-        return self._run_from(0, xh, parts)
+        return self._run_from(0, xh, self.parts if parts is None else parts)
+
+    def wait_compiled(self) -> "VGGEngine":
+        """Join the specialised kernels' compile jobs (and load them)."""
+        for st in self.steps:
+            if st.jit is not None:
+                st.jit.wait()
+        return self
 
     def _run_from(self, first: int, xin: torch.Tensor, parts: int = 2) -> torch.Tensor:
         """Layers first.. on xin (the input of layer ``first``), batch split over streams."""
@@ -152,11 +179,9 @@ class VGGEngine:
             lo, hi = n * j // parts, n * (j + 1) // parts
             with torch.cuda.stream(s):
                 cur, w = xin[lo:hi], w0
-                for st, out in zip(self.steps[first:], bufs[first:]):
+                for i, (st, out) in enumerate(zip(self.steps[first:], bufs[first:]), first):
                     # the parts run concurrently: the grid that must fill the GPU is the batch's
-                    bank, warps = st.plan_for(n)
-                    device.sf_conv3x3(cur, bank, st.bias, relu=True, pool=st.pool, out=out[lo:hi], w=w, ly=st.ly,
-                                      cta_warps=warps)
+                    st.conv(cur, out[lo:hi], w, n)
                     cur = out[lo:hi]
                     w = w // 2 if st.pool else w
         for s in streams:
@@ -204,10 +229,8 @@ class VGGEngine:
             cur.wait_event(ev)
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
-            bank, warps = first.plan_for(n)
-            device.sf_conv3x3(self._in[lo:hi], bank, first.bias, relu=True, pool=first.pool,
-                              out=bufs[0][lo:hi], w=self.hw, ly=first.ly, cta_warps=warps)
-        return device.halo_to_whc(self._run_from(1, bufs[0]), self.out_hw)
+            first.conv(self._in[lo:hi], bufs[0][lo:hi], self.hw, n)
+        return device.halo_to_whc(self._run_from(1, bufs[0], self.parts), self.out_hw)
 
     def run_exact(self, x: torch.Tensor) -> torch.Tensor:
         """Dense [N, C, H, W] -> [N, C', H', W'] through the reference-order kernels:

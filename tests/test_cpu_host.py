@@ -277,3 +277,50 @@ def test_weight_and_input_generators_match_reference():
         assert weights_sha(weights) == str(g[f"{key}__weights_sha"]), key
         x = prune_random(nw.random_input(net.input_dims, seed), 0.4, seed)
         assert x.to_array().tobytes() == g[f"{key}__x"].tobytes(), key
+
+
+def test_sfjit_generator_emits_valid_ptx_and_compiles():
+    """The per-layer code generator (csrc/sfjit.cu) on CPU: its PTX for both CTA modes
+    (parts of an image / whole images) assembles with ptxas, and the nvJitLink compile
+    jobs behind fscnn_sfjit_create finish without a GPU."""
+    import ctypes
+    import shutil
+    import subprocess
+    import tempfile
+
+    lib = _lib.load()
+    ptxas = shutil.which("ptxas") or "/usr/local/cuda/bin/ptxas"
+    rng = np.random.default_rng(0)
+    for c, k, h, pool in ((16, 40, 16, 1), (8, 32, 112, 0)):
+        w = (rng.standard_normal((k, c, 3, 3)) * 0.1).astype(np.float32)
+        w[rng.random(w.shape) < 0.9] = 0
+        b = rng.standard_normal(k).astype(np.float32)
+        g = 1 if k > 32 else 0  # the last (partial) group of 40 filters, or the only one
+        n = lib.fscnn_sfjit_ptx(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 0, g, None, 0)
+        assert n > 0
+        buf = ctypes.create_string_buffer(n + 1)
+        assert lib.fscnn_sfjit_ptx(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 0, g, buf, n + 1) == n
+        text = buf.value.decode()
+        assert ".entry sfjit" in text and "fma.rn.f32x2" in text
+        if os.path.exists(ptxas):
+            with tempfile.TemporaryDirectory() as d:
+                src = os.path.join(d, "g.ptx")
+                open(src, "w").write(text)
+                r = subprocess.run([ptxas, "-arch=sm_100a", "-O3", src, "-o", os.path.join(d, "g.cubin")],
+                                   capture_output=True, text=True)
+                assert r.returncode == 0, r.stderr[-2000:]
+        h_ = ctypes.c_void_p()
+        os.environ["FSCNN_JIT_CACHE"] = "off"
+        try:
+            assert lib.fscnn_sfjit_create(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 0, ctypes.byref(h_)) == 0
+            assert lib.fscnn_sfjit_compiled(h_) == 0, lib.fscnn_last_error()
+            info = (ctypes.c_int64 * 12)()
+            assert lib.fscnn_sfjit_info(h_, info, None) == 0
+            assert info[0] == -(-k // info[3])  # groups = ceil(k / filters per group)
+        finally:
+            del os.environ["FSCNN_JIT_CACHE"]
+            lib.fscnn_sfjit_destroy(h_)
+    # odd extents are refused with a message (the engine then keeps the jump-table kernel)
+    w = np.ones((8, 4, 3, 3), np.float32)
+    assert lib.fscnn_sfjit_ptx(w.ctypes.data, None, 8, 4, 15, 15, 1, 0, 0, 0, None, 0) == -1
+    assert b"even" in lib.fscnn_last_error()

@@ -407,3 +407,59 @@ def test_si_fast_at_vgg_layer_size(dev, layer, zf):
     s = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, dev.si_pack_fast(_t(wt + w2)), k)
     assert normwise_err(s.cpu().numpy(), (got + a).cpu().numpy()) <= FAST_TOL
     torch.cuda.synchronize()
+
+
+# -- per-layer specialised sparse-filter kernels (sfjit.cu) ----------------------------
+
+SFJIT_CASES = [
+    # c, k, h, n, relu, pool, zero fraction: part mode (large images, several CTAs per
+    # image), multi-image mode (small ones, ragged last CTA), partial filter groups,
+    # bias/ReLU/pool combinations, dense and nearly empty banks
+    (3, 8, 8, 1, True, False, 0.5),
+    (16, 32, 16, 2, True, True, 0.9),
+    (24, 40, 12, 3, False, False, 0.9),
+    (64, 64, 28, 5, True, True, 0.9),
+    (32, 64, 14, 33, True, False, 0.95),
+    (8, 32, 56, 2, True, True, 0.0),
+    (64, 32, 224, 1, True, False, 0.9),
+    (40, 72, 30, 2, True, True, 0.99),
+]
+
+
+@pytest.mark.parametrize("c,k,h,n,relu,pool,zf", SFJIT_CASES)
+def test_sfjit_bitwise_equals_jump_table_kernel(dev, oracle, c, k, h, n, relu, pool, zf):
+    """The specialised kernels accumulate in the jump-table kernel's order (channels
+    ascending, then each filter's taps), so the two agree bit for bit; both are checked
+    against the oracle at the north-star tolerance."""
+    rng = np.random.default_rng(c * 1000 + k + h)
+    w = (rng.standard_normal((k, c, 3, 3)) * 0.1).astype(np.float32)
+    w[rng.random(w.shape) < zf] = 0
+    b = (rng.standard_normal(k) * 0.1).astype(np.float32)
+    x = rng.standard_normal((n, c, h, h)).astype(np.float32)
+    xd = dev.to_halo(_t(x))
+    ref = dev.sf_conv3x3(xd, dev.sf_pack(_t(w)), _t(b), relu=relu, pool=pool, w=h)
+    got = dev.SfJit(w, b, h, h, relu=relu, pool=pool)(xd)
+    assert ref.cpu().numpy().tobytes() == got.cpu().numpy().tobytes()
+    if n * c * h * h <= 200_000:
+        nodes, seg = oracle.encode_bank(w)
+        want = oracle.sf_conv(x, nodes, seg, k, 3, 3, 1, 1, b)
+        if relu:
+            want = oracle.relu(want)
+        if pool:
+            want = oracle.pool(want, 2, 2, "max")
+        wo = h // 2 if pool else h
+        y = dev.from_halo(got, wo).cpu().numpy()
+        assert normwise_err(y, want) <= FAST_TOL
+
+
+def test_sfjit_batch_invariant(dev):
+    rng = np.random.default_rng(5)
+    c, k, h = 16, 64, 14
+    w = (rng.standard_normal((k, c, 3, 3)) * 0.1).astype(np.float32)
+    w[rng.random(w.shape) < 0.9] = 0
+    x = rng.standard_normal((7, c, h, h)).astype(np.float32)
+    j = dev.SfJit(w, None, h, h, relu=True, pool=True)
+    full = j(dev.to_halo(_t(x))).cpu().numpy()
+    for i in range(7):
+        one = j(dev.to_halo(_t(x[i : i + 1]))).cpu().numpy()
+        assert one.tobytes() == full[i : i + 1].tobytes()

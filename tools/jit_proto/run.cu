@@ -8,7 +8,8 @@
 #define CK(x) do { CUresult r_ = (x); if (r_ != CUDA_SUCCESS) { const char *s; cuGetErrorString(r_, &s); printf("%s:%d %s\n", __FILE__, __LINE__, s); exit(1);} } while (0)
 int main(int argc, char **argv) {
     const char *cub = argv[1];
-    int G = atoi(argv[2]); long long ffma_total = atoll(argv[3]); int ctas = atoi(argv[4]); int smem = atoi(argv[5]); int nt = argc > 6 ? atoi(argv[6]) : 128;
+    int G = atoi(argv[2]); long long ffma_total = atoll(argv[3]); int ctas = atoi(argv[4]); int smem = atoi(argv[5]); int nt = argc > 6 ? atoi(argv[6]) : 128; int flush = argc > 7 ? atoi(argv[7]) : 0;
+    void *fl = nullptr; if (flush) cudaMalloc(&fl, (size_t)512 << 20);
     cudaFree(0);
     CUmodule m; CK(cuModuleLoad(&m, cub));
     std::vector<CUfunction> f(G);
@@ -26,6 +27,7 @@ int main(int argc, char **argv) {
     std::vector<cudaEvent_t> done(G); for (auto &d : done) cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
     int tiles = 0;
     for (int rep = 0; rep < 4; ++rep) {
+        if (flush) cudaMemsetAsync(fl, rep, (size_t)512 << 20, 0);
         cudaEventRecord(e0, 0);
         for (int g = 0; g < G; ++g) {
             cudaStreamWaitEvent(st[g], e0, 0);
