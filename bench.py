@@ -425,6 +425,10 @@ def main():
                          "peak_source": "measured FFMA probe (fscnn_fp32_probe) on this GPU; "
                                         f"nominal 148x128x2x1.965GHz = {peak_nom:.1f}",
                          "frac_of_nominal": achieved_tf / peak_nom,
+                         "step_achieved": flops_img * n_total / (elapsed_ms / args.steps * 1e-3) / 1e12 / world,
+                         "step_frac": flops_img * n_total / (elapsed_ms / args.steps * 1e-3) / 1e12 / world / peak_meas,
+                         "step_note": "the timed step (4 batch parts on concurrent streams, replayed as one CUDA "
+                                      "graph) per GPU; 'achieved' is per-launch (each layer alone, full batch)",
                          "hbm_gbs_peak": peaks.get("hbm_gbs"),
                          "achieved_hbm_gbs": eng.bytes_per_image() * n_local / (kern_ms * 1e-3) / 1e9,
                          "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,

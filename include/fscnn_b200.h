@@ -53,6 +53,9 @@ const char *fscnn_last_error(void);
 /* Number of kernel launches this library issued since the last reset (host-side counter). */
 int64_t fscnn_launch_count(void);
 void fscnn_reset_launch_count(void);
+/* kernels replayed from a captured CUDA graph (the engine's forward) are not launched
+ * through the entry points; the host adds them here so the count stays complete */
+void fscnn_add_launch_count(int64_t n);
 
 /* ---------------------------------------------------------------------------
  * Encoder: dense -> node format.

@@ -29,6 +29,7 @@ _SIGNATURES = {
     "fscnn_last_error": (ctypes.c_char_p, []),
     "fscnn_launch_count": (_i64, []),
     "fscnn_reset_launch_count": (None, []),
+    "fscnn_add_launch_count": (None, [_i64]),
     "fscnn_encode_workspace_bytes": (_sz, [_i64]),
     "fscnn_encode_offsets": (_i32, [_vp] + [_i64] * 8 + [_vp, _vp, _vp, _sz, _vp]),
     "fscnn_encode_nodes": (_i32, [_vp] + [_i64] * 8 + [_vp, _vp, _vp, _vp, _vp]),

@@ -43,4 +43,6 @@ int64_t fscnn_launch_count(void) { return fscnn::g_launches.load(); }
 
 void fscnn_reset_launch_count(void) { fscnn::g_launches.store(0); }
 
+void fscnn_add_launch_count(int64_t n) { fscnn::g_launches.fetch_add(n); }
+
 }  // extern "C"

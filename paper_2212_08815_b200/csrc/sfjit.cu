@@ -166,6 +166,7 @@ struct Plan {
     int64_t stage_bytes;
     int64_t smem_bytes;
     int n_groups, n_chunks;
+    int odd_mode;  // kw = 1 pair: 0 = two 4-byte loads, 1 = moves from the even pairs
 };
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -194,7 +195,11 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         snprintf(why, why_n, "extents must be even (1x2 lane tiles, 2x2 pooling windows)");
         return false;
     }
-    p.KT = std::min(32, k);
+    p.odd_mode = getenv("FSCNN_SFJIT_ODD") ? atoi(getenv("FSCNN_SFJIT_ODD")) : 0;
+    // 48 filters per group: measured best on the VGG16 stack (32: -6 %, 64: -20 %; more
+    // filters per group = less code per FMA, fewer warps per CTA sharing its fetch)
+    p.KT = std::min(48, k);
+    if (getenv("FSCNN_SFJIT_KT")) p.KT = std::min(atoi(getenv("FSCNN_SFJIT_KT")), k);
     if (flags & 0xff) p.KT = std::min(flags & 0xff, k);
     p.TPR = w / 2, p.TPI = p.TPR * h;
     p.BW = 16;
@@ -458,15 +463,30 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
                 o("ld.shared.b64 e%d, [rb+%lld];", 2 * r, (long long)(off0 + (int64_t)r * p.P * 4));
                 o("ld.shared.b64 e%d, [rb+%lld];", 2 * r + 1, (long long)(off0 + (int64_t)r * p.P * 4 + 8));
             }
-            for (int r = 0; r < 3; ++r)
-                if (odd_row[r])
+            // the odd pair (columns 1, 2) for kw = 1 taps: two 4-byte loads straight into an
+            // aligned register pair (building it from the even pairs costs ptxas ~2.7x the
+            // two moves it needs: it rematerialises the pair per use)
+            for (int r = 0; r < 3; ++r) {
+                if (!odd_row[r] || p.odd_mode == 2) continue;
+                if (p.odd_mode == 0)
+                    o("{ .reg .f32 x1, x2; ld.shared.f32 x1, [rb+%lld]; ld.shared.f32 x2, [rb+%lld]; mov.b64 od%d, "
+                      "{x1, x2}; }",
+                      (long long)(off0 + (int64_t)r * p.P * 4 + 4), (long long)(off0 + (int64_t)r * p.P * 4 + 8), r);
+                else
                     o("{ .reg .f32 x0, x1, x2, x3; mov.b64 {x0, x1}, e%d; mov.b64 {x2, x3}, e%d; mov.b64 od%d, {x1, "
                       "x2}; }",
                       2 * r, 2 * r + 1, r);
+            }
             for (const Nz &z : nz) {
                 o("mov.b32 fw, 0f%08X;", z.w);
                 o("mov.b64 dw, {fw, fw};");
-                if (z.kw == 1)
+                if (z.kw == 1 && p.odd_mode == 2)
+                    // two scalar FMAs on the halves (columns 1 and 2 of the patch row)
+                    o("{ .reg .f32 x0, x1, x2, x3, s0, s1; mov.b64 {x0, x1}, e%d; mov.b64 {x2, x3}, e%d; "
+                      "mov.b64 {s0, s1}, a%d; fma.rn.f32 s0, x1, fw, s0; fma.rn.f32 s1, x2, fw, s1; "
+                      "mov.b64 a%d, {s0, s1}; }",
+                      2 * z.kh, 2 * z.kh + 1, z.kl, z.kl);
+                else if (z.kw == 1)
                     o("fma.rn.f32x2 a%d, od%d, dw, a%d;", z.kl, z.kh, z.kl);
                 else
                     o("fma.rn.f32x2 a%d, e%d, dw, a%d;", z.kl, 2 * z.kh + z.kw / 2, z.kl);

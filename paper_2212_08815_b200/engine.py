@@ -118,7 +118,16 @@ class VGGEngine:
         self.out_c, self.out_hw = c, h
         # batch split over streams: helps the jump-table kernel's partial last waves; the
         # specialised kernels already spread each layer over concurrent per-group launches
-        self.parts = 1 if all(st.jit is not None for st in self.steps) else 2
+        # batch split over concurrent streams: with the specialised kernels a layer's code
+        # is fetched from HBM by the first part and found in L2 by the others, and one
+        # part's partial last wave overlaps another's next layer (VGG16 @224, batch 32:
+        # 4.7 -> 4.1 ms with 4 parts, replayed as a graph; tools/stack_probe.py)
+        jit_all = all(st.jit is not None for st in self.steps)
+        self.parts = 4 if jit_all else 2
+        if os.environ.get("FSCNN_PARTS"):
+            self.parts = int(os.environ["FSCNN_PARTS"])
+        self.use_graphs = os.environ.get("FSCNN_GRAPHS", "1") != "0"
+        self._graphs = {}
         self._bufs = None
         self._bufs_batch = None
 
@@ -132,6 +141,7 @@ class VGGEngine:
                 ho = st.h // 2 if st.pool else st.h
                 bufs.append(device.halo_empty(n, st.k, ho, ho, dev))
             self._bufs, self._bufs_batch = bufs, n
+            self._graphs.clear()  # captured graphs point at the old buffers
         return self._bufs
 
     @property
@@ -152,7 +162,35 @@ class VGGEngine:
         stack at batch 32).  Results are identical (the kernels are batch-position
         invariant).
         """
-        return self._run_from(0, xh, self.parts if parts is None else parts)
+        return self._run(0, xh, self.parts if parts is None else parts)
+
+    def _run(self, first: int, xin: torch.Tensor, parts: int) -> torch.Tensor:
+        """_run_from through a CUDA graph captured once per (batch, entry layer, buffer):
+        a forward is ~13 x (groups + fork/join) launches, which the graph replays as one."""
+        if not self.use_graphs:
+            return self._run_from(first, xin, parts)
+        from . import _lib
+
+        key = (int(xin.shape[0]), first, parts, xin.data_ptr())
+        entry = self._graphs.get(key)
+        if entry is None:
+            cur = torch.cuda.current_stream()
+            self._run_from(first, xin, parts)  # eager warm-up: modules loaded, streams created
+            side = torch.cuda.Stream(device=xin.device)
+            side.wait_stream(cur)
+            g = torch.cuda.CUDAGraph()
+            n0 = _lib.launch_count()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    self._run_from(first, xin, parts)
+            kernels = _lib.launch_count() - n0
+            _lib.load().fscnn_add_launch_count(-kernels)  # captured, not launched
+            cur.wait_stream(side)
+            entry = self._graphs[key] = (g, kernels)
+        g, kernels = entry
+        g.replay()
+        _lib.load().fscnn_add_launch_count(kernels)
+        return self._bufs[-1]
 
     def wait_compiled(self) -> "VGGEngine":
         """Join the specialised kernels' compile jobs (and load them)."""
@@ -230,7 +268,7 @@ class VGGEngine:
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
             first.conv(self._in[lo:hi], bufs[0][lo:hi], self.hw, n)
-        return device.halo_to_whc(self._run_from(1, bufs[0], self.parts), self.out_hw)
+        return device.halo_to_whc(self._run(1, bufs[0], self.parts), self.out_hw)
 
     def run_exact(self, x: torch.Tensor) -> torch.Tensor:
         """Dense [N, C, H, W] -> [N, C', H', W'] through the reference-order kernels:

@@ -291,11 +291,11 @@ def test_sfjit_generator_emits_valid_ptx_and_compiles():
     lib = _lib.load()
     ptxas = shutil.which("ptxas") or "/usr/local/cuda/bin/ptxas"
     rng = np.random.default_rng(0)
-    for c, k, h, pool in ((16, 40, 16, 1), (8, 32, 112, 0)):
+    for c, k, h, pool in ((16, 72, 16, 1), (8, 32, 112, 0)):
         w = (rng.standard_normal((k, c, 3, 3)) * 0.1).astype(np.float32)
         w[rng.random(w.shape) < 0.9] = 0
         b = rng.standard_normal(k).astype(np.float32)
-        g = 1 if k > 32 else 0  # the last (partial) group of 40 filters, or the only one
+        g = 1 if k > 48 else 0  # the last (partial) group of 72 filters, or the only one
         n = lib.fscnn_sfjit_ptx(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 0, g, None, 0)
         assert n > 0
         buf = ctypes.create_string_buffer(n + 1)

@@ -55,23 +55,4 @@ def layer_times(reps_inner):
 print("in-stack once :", [round(v, 3) for v in layer_times(1)])
 print("hot x10       :", [round(v, 3) for v in layer_times(10)])
 
-# whole forward captured in a CUDA graph
-g = torch.cuda.CUDAGraph()
-s = torch.cuda.Stream()
-s.wait_stream(torch.cuda.current_stream())
-with torch.cuda.stream(s):
-    eng.run(xh)
-    torch.cuda.synchronize()
-    with torch.cuda.graph(g, stream=s):
-        eng.run(xh)
-torch.cuda.synchronize()
-for _ in range(3):
-    g.replay()
-torch.cuda.synchronize()
-a, b = ev(), ev()
-a.record()
-for _ in range(10):
-    g.replay()
-b.record()
-b.synchronize()
-print(f"graph stack: {a.elapsed_time(b) / 10:.3f} ms/step")
+# (forward_device already replays a CUDA graph per batch size: engine.VGGEngine._run)
