@@ -163,9 +163,14 @@ int fscnn_sf_pack_offsets(const float *w_kc33, int k, int c, int kt, int64_t *se
                           void *stream);
 int fscnn_sf_pack_nodes(const float *w_kc33, int k, int c, int kt, const int64_t *seg_off,
                         int64_t total_nodes, fscnn_node *nodes, void *stream);
-/* Fast conv.  x: [n][c][h][ldi] (ldi >= w, ldi % 4 == 0, 16-byte aligned; the
- * columns w..ldi-1 are never read).  y: [n][k][h][ldo], or with pool != 0 the fused
- * 2x2 max-pool result [n][k][h/2][ldo].  packed/packed_seg_off/total_nodes: the
+/* Fast conv on the HALO-COLUMN layout (not plain NCHW): logical column j of a row
+ * lives at memory column j + 1, memory column 0 must be zero (the TMA box that starts
+ * one column left of a tile reads it as the left padding) and memory columns > w are
+ * never read.  x: [n][c][h][ldi] with ldi >= w + 1, ldi % 4 == 0, 16-byte aligned.
+ * y: [n][k][h][ldo] in the same layout -- outputs written at memory columns 1..w,
+ * columns 0 and > w left untouched -- or with pool != 0 the fused 2x2 max-pool result
+ * [n][k][h/2][ldo] (columns 1..w/2); ldo even and y 8-byte aligned.  A plain NCHW
+ * tensor goes in and out with fscnn_pitch_copy (col 0 <-> col 1).  packed/packed_seg_off/total_nodes: the
  * packed stream (allocate total_nodes + 2 nodes: the kernel bulk-copies 16-byte
  * aligned ranges).  max_chunk_entries: the largest node count (sentinels included)
  * of any group over any run of `cc` consecutive channels.  ly selects the

@@ -554,6 +554,9 @@ int fscnn_sf_conv3x3_ex(const float *x, int n, int c, int h, int w, int ldi,
     FSCNN_REQUIRE(n > 0 && c > 0 && h > 0 && w > 0 && k > 0, "bad extents");
     FSCNN_REQUIRE(ldi >= w + 1 && ldi % 4 == 0, "input row pitch must be >= w + 1 and a multiple of 4");
     FSCNN_REQUIRE(ldo >= (pool ? w / 2 : w) + 1, "output row pitch too small");
+    // the non-pool epilogue stores a float2 at memory column x0 + 2 of each row
+    FSCNN_REQUIRE(ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(y) & 7) == 0,
+                  "output row pitch must be even and the output 8-byte aligned");
     FSCNN_REQUIRE(x && packed && packed_seg_off && y, "null buffer");
     FSCNN_REQUIRE(cc > 0 && cc <= 256, "bad channel chunk");
     FSCNN_REQUIRE(max_chunk_entries > 0, "bad entry capacity");

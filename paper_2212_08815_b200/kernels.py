@@ -100,9 +100,13 @@ def dense_from_device(y) -> DenseTensor3:
 
 
 def sparse_to_device(t: SparseTensor3):
-    """Host SparseTensor3 -> (device nodes, device segment offsets)."""
+    """Host SparseTensor3 -> (device nodes, device segment offsets).  The structure is
+    validated first (sorted in-range indices, sentinel-terminated segments): the kernels
+    trust it, and a malformed fiber would index shared memory out of bounds."""
     torch = _torch()
     from . import device
+
+    t.validate()
 
     return (device.nodes_from_numpy(t.nodes),
             torch.from_numpy(np.ascontiguousarray(t.segment_offsets, dtype=np.int64)).cuda())

@@ -22,6 +22,7 @@ from __future__ import annotations
 import math
 import struct
 import threading
+import weakref
 import time
 from dataclasses import dataclass, replace
 
@@ -308,7 +309,9 @@ class _Staging:
 
     def __init__(self):
         self.key = None
-        self.owned = []  # (base address, bytes, tensor) of pinned_batch buffers
+        # pinned_batch buffers by base address, held weakly: a buffer stays registered
+        # only while its DenseTensor3 views (or the caller) keep it alive
+        self.owned = weakref.WeakValueDictionary()
 
     def get(self, n, in_elems, out_elems):
         import torch
@@ -324,10 +327,10 @@ class _Staging:
         """The pinned tensor holding the batch back to back (zero-copy H2D), or None."""
         addr = [t.data.__array_interface__["data"][0] for t in batch]
         nbytes = elems * 4
-        for base, size, tensor in self.owned:
-            if addr[0] == base and len(batch) * nbytes <= size and all(
-                    a == base + i * nbytes for i, a in enumerate(addr)):
-                return tensor[: len(batch) * elems]
+        tensor = self.owned.get(addr[0])
+        if tensor is not None and len(batch) * nbytes <= tensor.numel() * 4 and all(
+                a == addr[0] + i * nbytes for i, a in enumerate(addr)):
+            return tensor[: len(batch) * elems]
         return None
 
 
@@ -348,7 +351,9 @@ def pinned_batch(n: int, dims) -> list:
     c, h, w = dims
     elems = c * h * w
     buf = torch.zeros(n * elems, dtype=torch.float32).pin_memory()
-    _staging.owned.append((buf.data_ptr(), buf.numel() * 4, buf))
+    _staging.owned[buf.data_ptr()] = buf
+    # the numpy views keep the pinned tensor alive (base chain), so the weak registry
+    # entry lives exactly as long as the returned batch
     arr = buf.numpy().reshape(n, elems)
     return [DenseTensor3((c, h, w), arr[i]) for i in range(n)]
 
