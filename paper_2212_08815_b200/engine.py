@@ -48,7 +48,7 @@ class ConvStep:
     def conv(self, x: torch.Tensor, out: torch.Tensor, w: int, n_plan: int) -> torch.Tensor:
         """conv3x3 + bias + ReLU [+ 2x2 max-pool] of a halo-column batch into ``out``:
         the specialised kernels when compiled, else the jump-table kernel (identical bits)."""
-        if self.jit is not None:
+        if self.jit is not None and n_plan >= SFJIT_MIN_BATCH:
             return self.jit(x, out=out)
         bank, warps = self.plan_for(n_plan)
         return device.sf_conv3x3(x, bank, self.bias, relu=True, pool=self.pool, out=out, w=w, ly=self.ly,
@@ -62,6 +62,13 @@ class ConvStep:
             if kt in self.small:
                 return self.small[kt], warps
         return self.bank, 0
+
+
+# Below this batch the jump-table kernel's small-grid plans win (a specialised kernel
+# CTA walks its group's whole code once however few tiles it has: VGG16 batch 1
+# 0.91 vs 1.46 ms, batch 8 2.30 vs 2.58; batch 16: 4.03 vs 3.10); the compiled code
+# does not depend on the batch, so both stay ready.
+SFJIT_MIN_BATCH = int(os.environ.get("FSCNN_SFJIT_MIN_BATCH", "12"))
 
 
 def _align4(v: int) -> int:
@@ -122,10 +129,7 @@ class VGGEngine:
         # is fetched from HBM by the first part and found in L2 by the others, and one
         # part's partial last wave overlaps another's next layer (VGG16 @224, batch 32:
         # 4.7 -> 4.1 ms with 4 parts, replayed as a graph; tools/stack_probe.py)
-        jit_all = all(st.jit is not None for st in self.steps)
-        self.parts = 4 if jit_all else 2
-        if os.environ.get("FSCNN_PARTS"):
-            self.parts = int(os.environ["FSCNN_PARTS"])
+        self._jit_all = all(st.jit is not None for st in self.steps)
         self.use_graphs = os.environ.get("FSCNN_GRAPHS", "1") != "0"
         self._graphs = {}
         self._bufs = None
@@ -162,7 +166,12 @@ class VGGEngine:
         stack at batch 32).  Results are identical (the kernels are batch-position
         invariant).
         """
-        return self._run(0, xh, self.parts if parts is None else parts)
+        return self._run(0, xh, self.parts_for(int(xh.shape[0])) if parts is None else parts)
+
+    def parts_for(self, n: int) -> int:
+        if os.environ.get("FSCNN_PARTS"):
+            return int(os.environ["FSCNN_PARTS"])
+        return 4 if self._jit_all and n >= SFJIT_MIN_BATCH else 2
 
     def _run(self, first: int, xin: torch.Tensor, parts: int) -> torch.Tensor:
         """_run_from through a CUDA graph captured once per (batch, entry layer, buffer):
@@ -268,7 +277,7 @@ class VGGEngine:
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
             first.conv(self._in[lo:hi], bufs[0][lo:hi], self.hw, n)
-        return device.halo_to_whc(self._run(1, bufs[0], self.parts), self.out_hw)
+        return device.halo_to_whc(self._run(1, bufs[0], self.parts_for(n)), self.out_hw)
 
     def run_exact(self, x: torch.Tensor) -> torch.Tensor:
         """Dense [N, C, H, W] -> [N, C', H', W'] through the reference-order kernels:

@@ -128,17 +128,22 @@ def _device_bank(filters: SparseTensor4):
     return entry
 
 
-def _fast_fills_gpu(dims, k: int) -> bool:
-    """The tiled fast kernel gives each CTA 512 outputs x 32 filters; for one small image
-    (BASELINE config 1: 56x56, 64 filters -> 16 CTAs) it leaves most of the 148 SMs idle
-    and the reference-order kernel (one thread per output and filter) is faster
-    (measured 13 vs 22 us, profiles/r01_configs_12.json) -- and bit-exact."""
+def _small_bank(filters: SparseTensor4, kt: int):
+    """The fast kernel's packed stream with ``kt`` filters per warp (cached with the bank)."""
+    import torch
+
     from . import device
 
-    c, h, w = dims
-    ly = device.pick_ly(c, h)
-    units = -(-(-(-h // (4 * ly)) * -(-w // 16)) // (8 // ly))
-    return units * -(-k // device.CTA_FILTERS) >= 148
+    hit = _bank_cache.get(("small", id(filters), kt))
+    if hit is not None and hit[0] is filters:
+        return hit[1]
+    nodes, seg, _ = _device_bank(filters)
+    k, c = filters.dims[:2]
+    dense = torch.empty((k, c, 3, 3), dtype=torch.float32, device="cuda")
+    device.decode(nodes, seg, k, 3, 3, c, dense, (c * 9, 1, 3, 9))
+    bank = device.sf_pack(dense, kt)
+    _bank_cache[("small", id(filters), kt)] = (filters, bank)
+    return bank
 
 
 def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: int, bias) -> DenseTensor3:
@@ -153,9 +158,14 @@ def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: 
     nodes, seg, packed = _device_bank(filters)
     b = torch.from_numpy(np.ascontiguousarray(bias, dtype=np.float32)).cuda()
     x = kernels.dense_to_device(t_in)
-    if packed is not None and stride == 1 and padding == 1 and not _EXACT and _fast_fills_gpu(t_in.dims, k):
+    if packed is not None and stride == 1 and padding == 1 and not _EXACT:
+        # the fast kernel, with its small-grid plan (fewer filters per warp, more CTAs)
+        # when the default grid would leave SMs idle -- one image of config 1: 11.9 us
+        # vs 13.2 for the reference-order kernel (profiles/r02_configs_12.json)
         c, h, w = t_in.dims
-        y = device.sf_conv3x3(device.to_halo(x), packed, b, relu=False, pool=False, w=w)
+        kt, warps = device.sf_grid_plan(1, h, w, k, device.pick_ly(c, h))
+        bank = packed if kt == packed.kt else _small_bank(filters, kt)
+        y = device.sf_conv3x3(device.to_halo(x), bank, b, relu=False, pool=False, w=w, cta_warps=warps)
         y = device.from_halo(y, w).contiguous()
     else:
         _, h_f, w_f = filters.dims[1:]

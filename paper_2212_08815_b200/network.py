@@ -493,8 +493,7 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
             elif variant == VARIANT_SPARSE_FILTER:
                 # the strategy I / II layer (layers._sf_layer), all images in one launch
                 nodes, seg, packed = ly._device_bank(step.params)
-                if packed is not None and (step.stride, step.padding) == (1, 1) and not ly._EXACT and \
-                        ly._fast_fills_gpu(dims, k):
+                if packed is not None and (step.stride, step.padding) == (1, 1) and not ly._EXACT:
                     y = device.sf_conv3x3(device.to_halo(x), packed, bias, relu=False, pool=False, w=dims[2])
                     y = device.from_halo(y, dims[2]).contiguous()
                 else:

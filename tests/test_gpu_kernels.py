@@ -463,3 +463,28 @@ def test_sfjit_batch_invariant(dev):
     for i in range(7):
         one = j(dev.to_halo(_t(x[i : i + 1]))).cpu().numpy()
         assert one.tobytes() == full[i : i + 1].tobytes()
+
+
+@pytest.mark.parametrize("layer", list(range(13)))
+def test_c4_sweep_points_against_exact_kernel(dev, layer):
+    """BASELINE config 4's sparse-filter points at batch 2: every VGG16 layer shape at
+    {50, 75, 90, 95, 99} % filter zeros, the fast jump-table kernel against the
+    reference-order exact kernel (pinned bit-exact to the reference) at the north-star
+    tolerance; the specialised kernels equal the jump-table kernel bit for bit on the
+    sparsest and densest points of a few shapes (their compile time is per bank)."""
+    import torch
+
+    c, k, h, w = wl.vgg16_conv_shapes()[layer]
+    for zf in (0.5, 0.75, 0.9, 0.95, 0.99):
+        x, wt, b = wl.sweep_layer(layer, "sf", zf, n=2)
+        wd, bias = _t(wt), _t(b)
+        xh = dev.to_halo(_t(x))
+        enc = dev.encode_order(wd, "CHW")
+        ex = dev.sf_conv_exact(_t(x), enc.nodes, enc.seg_off, k, 3, 3, 1, 1, bias, relu=True)
+        jt = dev.sf_conv3x3(xh, dev.sf_pack(wd), bias, relu=True, pool=False, w=w)
+        got = dev.from_halo(jt, w)
+        err = float((got - ex).abs().max() / ex.abs().max().clamp_min(1e-30))
+        assert err <= FAST_TOL, (layer, zf, err)
+        if layer in (0, 4, 12) and zf in (0.5, 0.99):
+            sj = dev.SfJit(wt, b, h, w, relu=True, pool=False)(xh)
+            assert torch.equal(sj.view(torch.int32), jt.view(torch.int32)), (layer, zf)

@@ -98,7 +98,11 @@ def main():
     bank_s = device.sf_pack(torch.from_numpy(wt).cuda(), kt)
     fast_small = lambda: device.sf_conv3x3(xh, bank_s, bias, False, False, out=out, w=56, cta_warps=warps)
     exact = lambda: device.sf_conv_exact(xd, enc.nodes, enc.seg_off, 64, 3, 3, 1, 1, bias)
-    for name, fn in (("fast", fast), ("fast_small_grid", fast_small), ("exact", exact)):
+    cases = [("fast", fast), ("fast_small_grid", fast_small), ("exact", exact)]
+    for kt in (4, 8, 16, 48):
+        j = device.SfJit(wt, b, 56, 56, relu=False, pool=False, flags=kt).wait()
+        cases.append((f"sfjit_kt{kt}", (lambda j=j: j(xh, out=out))))
+    for name, fn in cases:
         us, gus = per_call_us(fn), graph_us(fn)
         res[f"c1_{name}"] = {"us_per_call": us, "us_per_call_graph": gus, "nnz_gflop": fl / 1e9,
                              "nnz_gflops": fl / (gus * 1e-6) / 1e9}
