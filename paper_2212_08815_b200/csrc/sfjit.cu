@@ -167,6 +167,8 @@ struct Plan {
     int64_t smem_bytes;
     int n_groups, n_chunks;
     int odd_mode;  // kw = 1 pair: 0 = two 4-byte loads, 1 = moves from the even pairs
+    int tma_hint;  // 1: input boxes loaded L2 evict-first
+    int store_cs;  // 1: outputs stored streaming (evict-first)
 };
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -196,6 +198,8 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         return false;
     }
     p.odd_mode = getenv("FSCNN_SFJIT_ODD") ? atoi(getenv("FSCNN_SFJIT_ODD")) : 0;
+    p.tma_hint = getenv("FSCNN_SFJIT_TMA_HINT") ? atoi(getenv("FSCNN_SFJIT_TMA_HINT")) : 1;
+    p.store_cs = getenv("FSCNN_SFJIT_STORE_CS") ? atoi(getenv("FSCNN_SFJIT_STORE_CS")) : 1;
     // 48 filters per group: measured best on the VGG16 stack (32: -6 %, 64: -20 %; more
     // filters per group = less code per FMA, fewer warps per CTA sharing its fetch)
     p.KT = std::min(48, k);
@@ -404,8 +408,12 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
         o("add.u32 q2, rbar, %d;", 8 * s);
         o("mov.u32 q3, 0;");
         o("ISS%d:", j);
-        o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [qdst], [tm, "
-          "{q3, qy, qc, qimg}], [q2], pol;");
+        if (p.tma_hint)
+            o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [qdst], "
+              "[tm, {q3, qy, qc, qimg}], [q2], pol;");
+        else
+            o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [qdst], [tm, "
+              "{q3, qy, qc, qimg}], [q2];");
         o("add.u32 qdst, qdst, %lld;", (long long)p.box_bytes);
         o("add.u32 qimg, qimg, 1;");
         o("mov.u32 qy, -1;");
@@ -548,10 +556,10 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
             o("mov.b32 fm, 0fFF800000;");
             for (const char *v : {"f0", "f1", "g0", "g1"})
                 o("{ .reg .pred g; setp.gt.f32 g, %s, fm; selp.f32 fm, %s, fm, g; }", v, v);
-            o("@pv st.global.cs.f32 [yb], fm;");
+            o(p.store_cs ? "@pv st.global.cs.f32 [yb], fm;" : "@pv st.global.f32 [yb], fm;");
         } else {
-            o("@pv st.global.cs.f32 [yb], f0;");
-            o("@pv st.global.cs.f32 [yb+4], f1;");
+            o(p.store_cs ? "@pv st.global.cs.f32 [yb], f0;" : "@pv st.global.f32 [yb], f0;");
+            o(p.store_cs ? "@pv st.global.cs.f32 [yb+4], f1;" : "@pv st.global.f32 [yb+4], f1;");
         }
         if (kl + 1 < kn) o("add.u64 yb, yb, ks;");
     }
