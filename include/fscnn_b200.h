@@ -225,6 +225,13 @@ int fscnn_si_pack_fast(const float *w_kc33, int k, int c, float *wf, void *strea
 int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
                           int c, int h, int w, const float *wf, int k, const float *bias, float *y,
                           void *stream);
+/* Same with Alg. 7's pooling fused into the epilogue (layers.py:345-390): pool = 1 for a
+ * 2x2 max-pool, 2 for a 2x2 average-pool, applied to the conv output in
+ * _pool_dense_kernel's order (layers.py:250-271; as fscnn_pool2d) before + bias;
+ * y is [n][k][h/2][w/2] (h, w even).  pool = 0 is fscnn_si_conv3x3_fast. */
+int fscnn_si_conv3x3_fast_pool(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
+                               int c, int h, int w, const float *wf, int k, const float *bias, int pool,
+                               float *y, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Dense layers between convolutions.

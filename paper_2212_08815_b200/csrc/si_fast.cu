@@ -47,7 +47,8 @@ template <int TY, int TX, int NW, int KT>
 __global__ void __launch_bounds__(NW * 32, (TY * TX * KT <= 48 ? 24 : 16) / NW)
     si3x3_fast_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off,
                       int64_t n_nodes, int c_n, int h, int w, const float *__restrict__ wf, int k_n,
-                      int kp, int tiles_x, const float *__restrict__ bias, float *__restrict__ y) {
+                      int kp, int tiles_x, const float *__restrict__ bias, float *__restrict__ y,
+                      int pool) {
     using AccT = typename SiAcc<KT>::T;
     constexpr int RY = TY + 2, RX = TX + 2, NP = RY * RX, NWD = (NP + 31) / 32;
     __shared__ float val[kSiCC][NP];
@@ -181,6 +182,51 @@ __global__ void __launch_bounds__(NW * 32, (TY * TX * KT <= 48 ? 24 : 16) / NW)
             for (int t = 0; t < 9; ++t) wc[t] = wn[t];
         }
     }
+    if (pool) {
+        // Alg. 7 (layers.py:345-390): the conv output pooled 2x2 inside the tile (tiles
+        // sit at even coordinates), in pool2d's order -- (ph, pw) row-major, max from
+        // -inf with '>', avg as a left-to-right sum (first NaN wins) / 4 -- then + bias
+        const int ho = h >> 1, wo = w >> 1;
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int k = (grp * KT + j) * 32 + lane;
+            if (k >= k_n) continue;
+            const float bk = bias ? bias[k] : 0.0f;
+            float *yk = y + ((int64_t)img * k_n + k) * ho * wo;
+#pragma unroll
+            for (int qy = 0; qy < TY / 2; ++qy) {
+                const int yy = (ty0 >> 1) + qy;
+                if (yy >= ho) break;
+#pragma unroll
+                for (int qx = 0; qx < TX / 2; ++qx) {
+                    const int xx = (tx0 >> 1) + qx;
+                    if (xx >= wo) break;
+                    float m = pool == 1 ? -INFINITY : 0.0f;
+#pragma unroll
+                    for (int ph = 0; ph < 2; ++ph)
+#pragma unroll
+                        for (int pw = 0; pw < 2; ++pw) {
+                            const int o = (2 * qy + ph) * TX + 2 * qx + pw;
+                            float v;
+                            if constexpr (KT == 1)
+                                v = acc[o];
+                            else
+                                v = __uint_as_float((unsigned)(acc[o] >> (32 * j)));
+                            v = (v != 0.0f) ? v : 0.0f;
+                            if (pool == 1) {
+                                if (v > m) m = v;
+                            } else if (!is_nan_bits(m)) {
+                                m = is_nan_bits(v) ? nan_quiet(v) : __fadd_rn(m, v);
+                            }
+                        }
+                    if (pool == 2 && !is_nan_bits(m)) m = __fdiv_rn(m, 4.0f);
+                    if (bias) m = __fadd_rn(m, bk);
+                    yk[(int64_t)yy * wo + xx] = m;
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
         const int k = (grp * KT + j) * 32 + lane;
@@ -244,11 +290,11 @@ __global__ void si_pack_fast_kernel(const float *__restrict__ w, int k_n, int c_
 
 template <int TY, int TX, int NW, int KT>
 int launch_fast(const int2 *nodes, const int64_t *seg_off, int64_t n_nodes, int n, int c, int h, int w,
-                const float *wf, int k, int kp, const float *bias, float *y, cudaStream_t st) {
+                const float *wf, int k, int kp, const float *bias, float *y, cudaStream_t st, int pool) {
     const int tiles_x = (int)ceil_div(w, TX), tiles_y = (int)ceil_div(h, TY);
     dim3 grid((unsigned)(tiles_x * tiles_y), (unsigned)ceil_div(kp, NW * 32 * KT), (unsigned)n);
     si3x3_fast_kernel<TY, TX, NW, KT><<<grid, NW * 32, 0, st>>>(nodes, seg_off, n_nodes, c, h, w, wf, k, kp,
-                                                                tiles_x, bias, y);
+                                                                tiles_x, bias, y, pool);
     FSCNN_LAUNCH_CHECK("si3x3_fast_kernel");
     return FSCNN_OK;
 }
@@ -275,9 +321,11 @@ int fscnn_si_pack_fast(const float *w_kc33, int k, int c, float *wf, void *strea
     return FSCNN_OK;
 }
 
-int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
-                          int c, int h, int w, const float *wf, int k, const float *bias, float *y,
-                          void *stream) {
+int fscnn_si_conv3x3_fast_pool(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
+                               int c, int h, int w, const float *wf, int k, const float *bias, int pool,
+                               float *y, void *stream) {
+    FSCNN_REQUIRE(pool >= 0 && pool <= 2, "pool must be 0 (none), 1 (2x2 max) or 2 (2x2 avg)");
+    if (pool) FSCNN_REQUIRE(h % 2 == 0 && w % 2 == 0, "fused 2x2 pool needs even extents");
     FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0 && n_nodes >= 0, "bad extents");
     if (n == 0 || k == 0) return FSCNN_OK;
     FSCNN_REQUIRE(in_nodes && in_seg_off && wf && y, "null buffer");
@@ -287,14 +335,20 @@ int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off,
     const int2 *nd = reinterpret_cast<const int2 *>(in_nodes);
     cudaStream_t st = as_stream(stream);
     if (kt == 2) {
-        if (nw == 8) return launch_fast<4, 8, 8, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
-        if (nw == 4) return launch_fast<4, 8, 4, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
-        return launch_fast<4, 8, 2, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
+        if (nw == 8) return launch_fast<4, 8, 8, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+        if (nw == 4) return launch_fast<4, 8, 4, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+        return launch_fast<4, 8, 2, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
     }
     // one filter per lane (K < 128)
-    if (nw == 8) return launch_fast<4, 8, 8, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
-    if (nw == 4) return launch_fast<4, 8, 4, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
-    return launch_fast<4, 8, 2, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st);
+    if (nw == 8) return launch_fast<4, 8, 8, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+    if (nw == 4) return launch_fast<4, 8, 4, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+    return launch_fast<4, 8, 2, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+}
+
+int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
+                          int c, int h, int w, const float *wf, int k, const float *bias, float *y,
+                          void *stream) {
+    return fscnn_si_conv3x3_fast_pool(in_nodes, in_seg_off, n_nodes, n, c, h, w, wf, k, bias, 0, y, stream);
 }
 
 }  // extern "C"

@@ -506,14 +506,17 @@ def si_use_fast(h: int, w: int, k: int) -> bool:
 
 def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,
                     wf: torch.Tensor, k: int, bias: torch.Tensor | None = None,
-                    out: torch.Tensor | None = None) -> torch.Tensor:
+                    out: torch.Tensor | None = None, pool: str | None = None) -> torch.Tensor:
     """3x3/s1/p1 sparse-input conv, channel-major (fp32 reassociation of kernels.py:136-166,
-    held to the north-star 1e-4 normwise tolerance)."""
+    held to the north-star 1e-4 normwise tolerance).  ``pool`` = 'max' / 'avg' fuses
+    Alg. 7's 2x2 pooling (layers.py:345-390) into the epilogue: [n, k, h/2, w/2]."""
+    mode = {None: 0, "max": 1, "avg": 2}[pool]
     if out is None:
-        out = torch.empty((n, k, h, w), dtype=torch.float32, device=nodes.device)
+        shape = (n, k, h // 2, w // 2) if mode else (n, k, h, w)
+        out = torch.empty(shape, dtype=torch.float32, device=nodes.device)
     n_nodes = int(nodes.numel() // 2)
-    call("fscnn_si_conv3x3_fast", ptr(nodes), ptr(seg_off), n_nodes, n, c, h, w, ptr(wf), k, ptr(bias), ptr(out),
-         stream())
+    call("fscnn_si_conv3x3_fast_pool", ptr(nodes), ptr(seg_off), n_nodes, n, c, h, w, ptr(wf), k, ptr(bias), mode,
+         ptr(out), stream())
     return out
 
 

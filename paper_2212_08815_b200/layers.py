@@ -188,7 +188,10 @@ def conv_forward_strategy_II(t_in: DenseTensor3, filters: SparseTensor4, stride:
 # -- sparse-input conv layer ----------------------------------------------------------
 
 
-def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, padding: int):
+def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, padding: int,
+              fused_pool=None, pool_mode: str = POOL_MAX):
+    """The conv on the device; with a 2x2 ``fused_pool`` on the channel-major path the
+    pool runs in the kernel's epilogue (Alg. 7) and the result is already pooled."""
     from . import device
 
     if t_in.order is not AxisOrder3.CHW:
@@ -200,7 +203,11 @@ def _si_dense(t_in: SparseTensor3, filters: list[DenseTensor3], stride: int, pad
     kcrs = kernels.filters_to_device_kcrs(filters)
     k = len(filters)
     if (h_f, w_f, stride, padding) == (3, 3, 1, 1) and not _EXACT and device.si_use_fast(h, w, k):
-        y = device.si_conv3x3_fast(nodes, seg, 1, c, h, w, device.si_pack_fast(kcrs), k)
+        fp = None
+        if fused_pool is not None and tuple(fused_pool) == (2, 2) and h % 2 == 0 and w % 2 == 0 and \
+                pool_mode in (POOL_MAX, POOL_AVG):
+            fp = "max" if pool_mode == POOL_MAX else "avg"
+        y = device.si_conv3x3_fast(nodes, seg, 1, c, h, w, device.si_pack_fast(kcrs), k, pool=fp)
     elif (h_f, w_f, stride, padding) == (3, 3, 1, 1):
         y = device.si_conv3x3(nodes, seg, 1, c, h, w, device.si_pack3x3(kcrs), len(filters))
     else:
@@ -228,8 +235,11 @@ def conv_forward_sparse_input(t_in: SparseTensor3, filters: list[DenseTensor3], 
 
     from . import device
 
-    y, geom = _si_dense(t_in, filters, stride, padding)
-    if fused_pool is not None:
+    if fused_pool is not None:  # validate the window before any device work
+        g0 = ConvGeometry(tuple(t_in.dims), tuple(filters[0].dims), stride, padding)
+        _pool_args(fused_pool, pool_mode, g0.n_h, g0.n_w)
+    y, geom = _si_dense(t_in, filters, stride, padding, fused_pool, pool_mode)
+    if fused_pool is not None and tuple(y.shape[2:]) == (geom.n_h, geom.n_w):
         h_p, w_p = _pool_args(fused_pool, pool_mode, geom.n_h, geom.n_w)
         y = device.pool2d(y, h_p, w_p, pool_mode == POOL_MAX)
     bias = np.asarray(bias, dtype=np.float32)

@@ -476,15 +476,23 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
             if sparse:
                 enc = device.encode_order(x, "CHW")
                 _, ci, hi, wi = (int(v) for v in x.shape)
+                fused = False
                 if (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1) and not ly._EXACT and \
                         device.si_use_fast(hi, wi, k):
-                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack_fast(kcrs), k)
+                    # Alg. 7 in the kernel's epilogue when the fused pool is 2x2 (VGG16's)
+                    fp = None
+                    if step.fused_pool is not None and tuple(step.fused_pool) == (2, 2) and hi % 2 == 0 \
+                            and wi % 2 == 0:
+                        fp = "max" if step.fused_pool_mode == ly.POOL_MAX else "avg"
+                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack_fast(kcrs), k,
+                                               pool=fp)
+                    fused = fp is not None
                 elif (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
                     y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack3x3(kcrs), k)
                 else:
                     y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, device.kcrs_to_crsk(kcrs), k, h_f,
                                        w_f, step.stride, step.padding)
-                if step.fused_pool is not None:
+                if step.fused_pool is not None and not fused:
                     h_p, w_p = ly._pool_args(step.fused_pool, step.fused_pool_mode, geom.n_h, geom.n_w)
                     y = device.pool2d(y, h_p, w_p, step.fused_pool_mode == ly.POOL_MAX)
                 if np.any(step.bias != 0):

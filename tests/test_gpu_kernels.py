@@ -488,3 +488,26 @@ def test_c4_sweep_points_against_exact_kernel(dev, layer):
         if layer in (0, 4, 12) and zf in (0.5, 0.99):
             sj = dev.SfJit(wt, b, h, w, relu=True, pool=False)(xh)
             assert torch.equal(sj.view(torch.int32), jt.view(torch.int32)), (layer, zf)
+
+
+@pytest.mark.parametrize("mode", ["max", "avg"])
+def test_si_fast_fused_pool_equals_conv_then_pool(dev, mode):
+    """Alg. 7 in the channel-major kernel's epilogue (layers.py:345-390) gives exactly the
+    conv followed by the standalone pool (_pool_dense_kernel order), bias added after."""
+    import torch
+
+    rng = np.random.default_rng(17 if mode == "max" else 18)
+    for n, c, k, h, w in ((2, 40, 72, 12, 20), (1, 128, 128, 28, 28), (3, 16, 200, 10, 14)):
+        x = np.abs(rng.standard_normal((n, c, h, w))).astype(np.float32)
+        x[rng.random(x.shape) < 0.85] = 0
+        if mode == "max":
+            x[0, 0, 1, 1] = -0.0  # explicit -0.0 inputs behave like absent nodes
+        wt = (rng.standard_normal((k, c, 3, 3)) * 0.05).astype(np.float32)
+        b = (rng.standard_normal(k) * 0.01).astype(np.float32)
+        enc = dev.encode_order(_t(x), "CHW")
+        wf = dev.si_pack_fast(_t(wt))
+        conv = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, wf, k)
+        want = dev.pool2d(conv, 2, 2, mode == "max") + _t(b).view(1, -1, 1, 1)
+        got = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, wf, k, bias=_t(b), pool=mode)
+        assert tuple(got.shape) == (n, k, h // 2, w // 2)
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (n, c, k, h, w)
