@@ -280,7 +280,8 @@ int fscnn_nchw_to_whc_ex(const float *x, int n, int c, int h, int w, int ld, int
  * order, so its outputs are bit-identical to fscnn_sf_conv3x3_ex's.
  *   create: w_kc33 = dense host bank [k][c][3][3] (+-0.0 entries are absent nodes),
  *           bias = host [k] or NULL; h, w even; flags: bits 0-7 filters per group
- *           (0 = 32), bits 8-15 warps per CTA (0 = 12).  Returns immediately: the
+ *           (0 = 48), bits 8-15 a cap on warps per CTA (0 = none), bit 16: one fused
+ *           kernel for all groups (small layers: one launch).  Returns immediately: the
  *           compile runs in the background; wait (or the first launch) joins it.
  *   launch: x = halo-column input [n][c][h][ldi] (logical column j at memory column j+1,
  *           column 0 zero, ldi >= w+1 and a multiple of 4, 16-byte aligned);

@@ -166,6 +166,7 @@ struct Plan {
     int64_t stage_bytes;
     int64_t smem_bytes;
     int n_groups, n_chunks;
+    int fused;     // 1: one kernel for all groups (grid.y = group), one compile job
     int odd_mode;  // kw = 1 pair: 0 = two 4-byte loads, 1 = moves from the even pairs
     int tma_hint;  // 1: input boxes loaded L2 evict-first
     int store_cs;  // 1: outputs stored streaming (evict-first)
@@ -267,6 +268,7 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         return false;
     }
     p.n_groups = (k + p.KT - 1) / p.KT;
+    p.fused = (flags >> 16) & 1;
     p.n_chunks = (c + p.CC - 1) / p.CC;
     return true;
 }
@@ -294,12 +296,16 @@ uint32_t fbits(float v) {
 }
 
 // wt: dense [K][C][3][3] fp32 (host), bias [K] (host, may be null)
-std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) {
+// gen_group: one group's standalone kernel; gen_fused: one kernel for every group of
+// the layer (blockIdx.y = group, a jump table to the group's code) -- small layers,
+// where one launch beats a fork over per-group launches.
+std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_first, int g_count) {
     Out o;
     o.s.reserve(1 << 20);
     const int KT = p.KT;
-    const int k0 = g * KT;
-    const int kn = std::min(KT, p.K - k0);
+    const bool fused = g_count > 1;
+    int kn = 0;
+    for (int g = g_first; g < g_first + g_count; ++g) kn = std::max(kn, std::min(KT, p.K - g * KT));
     const int U = 2 * p.TPR;  // tiles per row pair
     o(".version 8.7");
     o(".target sm_100a");
@@ -392,6 +398,7 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
     for (int s = 0; s < p.S; ++s) o("mbarrier.init.shared::cta.b64 [rbar+%d], 1;", 8 * s);
     o("fence.mbarrier_init.release.cluster;");
     o("prefetch.tensormap [tm];");
+    std::string lp = "p_";  // label prefix: prologue, then one per group
     auto issue = [&](int j) {
         const int s = j % p.S;
         const int c0 = j * p.CC;
@@ -407,7 +414,7 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
         o("mov.u32 qbi, 0;");
         o("add.u32 q2, rbar, %d;", 8 * s);
         o("mov.u32 q3, 0;");
-        o("ISS%d:", j);
+        o("%sISS%d:", lp.c_str(), j);
         if (p.tma_hint)
             o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [qdst], "
               "[tm, {q3, qy, qc, qimg}], [q2], pol;");
@@ -419,34 +426,44 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
         o("mov.u32 qy, -1;");
         o("add.u32 qbi, qbi, 1;");
         o("setp.lt.u32 pl, qbi, nbox;");
-        o("@pl bra ISS%d;", j);
+        o("@pl bra %sISS%d;", lp.c_str(), j);
     };
     for (int j = 0; j < std::min(p.S, p.n_chunks); ++j) issue(j);
     o("PRO_DONE:");
     o("barrier.sync 0;");
     for (int i = 0; i < kn; ++i) o("mov.b64 a%d, 0;", i);
-
-    // ---- channel chunks
+    if (fused) {
+        std::string t = "GTBL: .branchtargets ";
+        for (int g = g_first; g < g_first + g_count; ++g) t += (g > g_first ? ", G" : "G") + std::to_string(g);
+        o.s += t + ";\n";
+        o("{ .reg .b32 gy; mov.u32 gy, %%ctaid.y; brx.idx.uni gy, GTBL; }");
+    }
     struct Nz {
         int kl, kh, kw;
         uint32_t w;
     };
     std::vector<Nz> nz;
     nz.reserve(9 * 64);
+  for (int g = g_first; g < g_first + g_count; ++g) {
+    const int k0 = g * KT;
+    const int kn = std::min(KT, p.K - k0);
+    lp = "g" + std::to_string(g) + "_";
+    if (fused) o("G%d:", g);
+    // ---- channel chunks
     for (int j = 0; j < p.n_chunks; ++j) {
         const int s = j % p.S;
         const int par_bit = (j / p.S) & 1;
         // bounded wait: a stage that never completes traps instead of hanging the GPU
         o("mov.u32 q4, %d;", par_bit);
         o("mov.u32 q3, 0;");
-        o("WT%d:", j);
+        o("%sWT%d:", lp.c_str(), j);
         o("mbarrier.try_wait.parity.shared::cta.b64 pw, [rbar+%d], q4;", 8 * s);
-        o("@pw bra WD%d;", j);
+        o("@pw bra %sWD%d;", lp.c_str(), j);
         o("add.u32 q3, q3, 1;");
         o("setp.gt.u32 pl, q3, 4000000;");
         o("@pl trap;");
-        o("bra.uni WT%d;", j);
-        o("WD%d:", j);
+        o("bra.uni %sWT%d;", lp.c_str(), j);
+        o("%sWD%d:", lp.c_str(), j);
         const int cend = std::min(p.C, (j + 1) * p.CC);
         for (int c = j * p.CC; c < cend; ++c) {
             const int cl = c - j * p.CC;
@@ -503,9 +520,9 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
         if (j + p.S < p.n_chunks) {
             // every warp is done with stage s: thread 0 restages it with chunk j+S
             o("barrier.sync 0;");
-            o("@!pt0 bra RS%d;", j);
+            o("@!pt0 bra %sRS%d;", lp.c_str(), j);
             issue(j + p.S);
-            o("RS%d:", j);
+            o("%sRS%d:", lp.c_str(), j);
         }
     }
 
@@ -564,8 +581,13 @@ std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) 
         if (kl + 1 < kn) o("add.u64 yb, yb, ks;");
     }
     o("ret;");
+  }
     o("}");
     return o.s;
+}
+
+std::string gen_group(const Plan &p, const float *wt, const float *bias, int g) {
+    return gen_kernel(p, wt, bias, g, 1);
 }
 
 uint64_t fnv1a(const std::string &s, uint64_t h = 1469598103934665603ull) {
@@ -631,6 +653,10 @@ struct fscnn_sfjit {
     std::vector<cudaStream_t> streams;
     std::vector<cudaEvent_t> done;
     cudaEvent_t fork = nullptr;
+    // the last input's tensor map (encoding one costs ~1 us of host time per launch)
+    const float *map_x = nullptr;
+    int map_n = 0, map_ldi = 0;
+    CUtensorMap map;
     std::vector<fscnn::Group> groups;
     std::mutex mu;
     std::condition_variable cv;
@@ -655,8 +681,9 @@ int fscnn_sfjit_create(const float *w_kc33, const float *bias, int k, int c, int
         return FSCNN_ERR_UNSUPPORTED;
     }
     const Plan &p = j->plan;
-    j->groups.resize(p.n_groups);
-    j->pending = p.n_groups;
+    const int n_jobs = p.fused ? 1 : p.n_groups;
+    j->groups.resize(n_jobs);
+    j->pending = n_jobs;
     const auto t0 = std::chrono::steady_clock::now();
     // weights are copied for the background generators (the caller's buffers may go away)
     auto wt = std::make_shared<std::vector<float>>(w_kc33, w_kc33 + (int64_t)k * c * 9);
@@ -665,11 +692,14 @@ int fscnn_sfjit_create(const float *w_kc33, const float *bias, int k, int c, int
     const std::string dir = cache_dir();
     const bool use_cache = !(getenv("FSCNN_JIT_CACHE") && std::string(getenv("FSCNN_JIT_CACHE")) == "off");
     fscnn_sfjit *raw = j.get();
-    for (int g = 0; g < p.n_groups; ++g) {
+    for (int g = 0; g < n_jobs; ++g) {
         Pool::get().submit([raw, g, wt, bs, dir, use_cache] {
             Group &G = raw->groups[g];
             const auto s0 = std::chrono::steady_clock::now();
-            const std::string ptx = gen_group(raw->plan, wt->data(), bs->empty() ? nullptr : bs->data(), g);
+            const Plan &pl = raw->plan;
+            const std::string ptx = pl.fused ? gen_kernel(pl, wt->data(), bs->empty() ? nullptr : bs->data(), 0,
+                                                          pl.n_groups)
+                                             : gen_group(pl, wt->data(), bs->empty() ? nullptr : bs->data(), g);
             char name[64];
             snprintf(name, sizeof(name), "/%016llx.cubin", (unsigned long long)fnv1a(ptx));
             const std::string path = dir + name;
@@ -762,24 +792,41 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
     FSCNN_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, "input must be 16-byte aligned");
     FSCNN_REQUIRE((int64_t)n * p.M < (1ll << 31), "batch too large");
     const Driver &d = driver();
-    CUtensorMap map;
-    cuuint64_t gdim[4] = {(cuuint64_t)p.W + 1, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)n};
-    cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * p.H * 4, (cuuint64_t)ldi * p.H * p.C * 4};
-    cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)p.CC, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = d.encodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride, box,
-                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("sfjit: cuTensorMapEncodeTiled failed (%s)", cu_err(r));
-        return FSCNN_ERR_CUDA;
+    CUresult r = CUDA_SUCCESS;
+    if (x != j->map_x || n != j->map_n || ldi != j->map_ldi) {
+        cuuint64_t gdim[4] = {(cuuint64_t)p.W + 1, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)n};
+        cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * p.H * 4, (cuuint64_t)ldi * p.H * p.C * 4};
+        cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)p.CC, 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        r = d.encodeTiled(&j->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride, box,
+                          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            j->map_x = nullptr;
+            set_error("sfjit: cuTensorMapEncodeTiled failed (%s)", cu_err(r));
+            return FSCNN_ERR_CUDA;
+        }
+        j->map_x = x, j->map_n = n, j->map_ldi = ldi;
     }
+    CUtensorMap &map = j->map;
     const unsigned grid = p.MODE == 0 ? (unsigned)(n * p.M) : (unsigned)((n + p.Q - 1) / p.Q);
     uint32_t ldo_u = (uint32_t)ldo, nt_u = (uint32_t)n;
     // The groups are independent kernels over the same input: fork them over side
     // streams so they share the GPU (one group's grid alone leaves SMs idle on the deep
     // layers), join back on the caller's stream.  Stream-ordered and graph-capturable.
     cudaStream_t cs = as_stream(stream);
+    if (p.fused) {
+        float *yg = y;
+        void *args[] = {&map, &yg, &ldo_u, &nt_u};
+        r = d.launchKernel(j->groups[0].fn, grid, (unsigned)p.n_groups, 1, (unsigned)p.T, 1, 1,
+                           (unsigned)p.smem_bytes, reinterpret_cast<CUstream>(stream), args, nullptr);
+        if (r != CUDA_SUCCESS) {
+            set_error("sfjit launch: %s", cu_err(r));
+            return FSCNN_ERR_CUDA;
+        }
+        note_launch(1);
+        return FSCNN_OK;
+    }
     const int n_side = (int)std::min<size_t>(j->groups.size(), 16);
     if (n_side > 1 && (int)j->streams.size() < n_side) {
         if (!j->fork && cudaEventCreateWithFlags(&j->fork, cudaEventDisableTiming) != cudaSuccess) {

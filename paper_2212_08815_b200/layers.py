@@ -128,6 +128,32 @@ def _device_bank(filters: SparseTensor4):
     return entry
 
 
+_LAYER_JIT = os.environ.get("FSCNN_LAYER_JIT", "1") != "0"
+_jit_cache: dict = {}
+
+
+def _layer_jit(filters: SparseTensor4, bias, h: int, w: int):
+    """The single-kernel specialised conv of a bank (+ bias, no ReLU/pool), cached."""
+    import torch
+
+    from . import device
+
+    b = np.ascontiguousarray(bias, dtype=np.float32)
+    key = (id(filters), b.tobytes(), h, w)
+    hit = _jit_cache.get(key)
+    if hit is not None and hit[0] is filters:
+        return hit[1]
+    nodes, seg, _ = _device_bank(filters)
+    k, c = filters.dims[:2]
+    dense = torch.empty((k, c, 3, 3), dtype=torch.float32, device="cuda")
+    device.decode(nodes, seg, k, 3, 3, c, dense, (c * 9, 1, 3, 9))
+    jit = device.SfJit(dense, b, h, w, relu=False, pool=False, flags=4 | (8 << 8) | (1 << 16))
+    if len(_jit_cache) > 32:
+        _jit_cache.clear()
+    _jit_cache[key] = (filters, jit)
+    return jit
+
+
 def _small_bank(filters: SparseTensor4, kt: int):
     """The fast kernel's packed stream with ``kt`` filters per warp (cached with the bank)."""
     import torch
@@ -158,11 +184,21 @@ def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: 
     nodes, seg, packed = _device_bank(filters)
     b = torch.from_numpy(np.ascontiguousarray(bias, dtype=np.float32)).cuda()
     x = kernels.dense_to_device(t_in)
+    c, h, w = t_in.dims
+    if packed is not None and stride == 1 and padding == 1 and not _EXACT and h % 2 == 0 and w % 2 == 0 \
+            and device.sfjit_enabled() and _LAYER_JIT:
+        # one layer call = one image: the bank compiled into ONE specialised kernel
+        # (4 filters per group, blockIdx.y = group, 8-warp CTAs) -- config 1: 3.8 us
+        # graph-launched vs 11.9 for the jump-table kernel's small-grid plan and 13.2 for
+        # the reference-order kernel (profiles/r02_configs_12.json); bit-identical to
+        # the jump-table kernel.  Compiled on first use, cached with the bank.
+        jit = _layer_jit(filters, bias, h, w)
+        y = device.from_halo(jit(device.to_halo(x)), w).contiguous()
+        return kernels.dense_from_device(y)
     if packed is not None and stride == 1 and padding == 1 and not _EXACT:
         # the fast kernel, with its small-grid plan (fewer filters per warp, more CTAs)
         # when the default grid would leave SMs idle -- one image of config 1: 11.9 us
         # vs 13.2 for the reference-order kernel (profiles/r02_configs_12.json)
-        c, h, w = t_in.dims
         kt, warps = device.sf_grid_plan(1, h, w, k, device.pick_ly(c, h))
         bank = packed if kt == packed.kt else _small_bank(filters, kt)
         y = device.sf_conv3x3(device.to_halo(x), bank, b, relu=False, pool=False, w=w, cta_warps=warps)

@@ -102,6 +102,9 @@ def main():
     for kt in (4, 8, 16, 48):
         j = device.SfJit(wt, b, 56, 56, relu=False, pool=False, flags=kt).wait()
         cases.append((f"sfjit_kt{kt}", (lambda j=j: j(xh, out=out))))
+    for kt, wc in ((2, 0), (4, 0), (8, 0), (16, 0), (4, 8), (8, 8), (16, 8)):
+        j = device.SfJit(wt, b, 56, 56, relu=False, pool=False, flags=kt | (wc << 8) | (1 << 16)).wait()
+        cases.append((f"sfjit_fused_kt{kt}_w{wc}", (lambda j=j: j(xh, out=out))))
     for name, fn in cases:
         us, gus = per_call_us(fn), graph_us(fn)
         res[f"c1_{name}"] = {"us_per_call": us, "us_per_call_graph": gus, "nnz_gflop": fl / 1e9,

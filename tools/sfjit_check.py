@@ -37,6 +37,9 @@ def main():
     cases = [(3, 8, 8, 1, True, False), (16, 32, 16, 2, True, True), (24, 40, 12, 3, False, False),
              (64, 64, 28, 5, True, True), (32, 64, 14, 33, True, False), (8, 32, 56, 2, True, True),
              (64, 32, 224, 1, True, False)]
+    cases = [cs + (0.9, 0, 0) for cs in cases] + [
+        (64, 64, 56, 1, False, False, 0.95, 0, 8 | (1 << 16)), (24, 40, 12, 3, True, True, 0.9, 0, 4 | (1 << 16)),
+        (16, 72, 28, 2, True, False, 0.8, 0, 16 | (8 << 8) | (1 << 16))]
     ok = True
     for cs in cases:
         same, dt, info, (ref, got) = run_pair(*cs)
