@@ -156,7 +156,8 @@ struct Plan {
     int KT, WARPS, T;   // filters per group, warps per CTA, threads per CTA (32*WARPS)
     int MODE;           // 0: M CTAs per image (TI tiles each), 1: Q whole images per CTA
     int M, Q, TI;
-    int TPR, TPI;       // tiles per row (w/2), per image (h * w/2)
+    int TPR, TPI;       // tiles per row (w/2, padded to a multiple of 8 when odd), per image
+    int TPRR;           // real tiles per row (w/2): lanes past it compute nothing they store
     int BW;             // column block of the lane order (pool partner = lane ^ BW)
     int P;              // smem row pitch (floats) == TMA box width
     int BH;             // TMA box rows
@@ -206,13 +207,23 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     p.KT = std::min(48, k);
     if (getenv("FSCNN_SFJIT_KT")) p.KT = std::min(atoi(getenv("FSCNN_SFJIT_KT")), k);
     if (flags & 0xff) p.KT = std::min(flags & 0xff, k);
-    p.TPR = w / 2, p.TPI = p.TPR * h;
+    // an odd tile-row length (w = 14: 7 tiles) would pair rows of a pooling window in a
+    // column block of 1, whose 8-byte patch loads collide on banks at every row-pair
+    // wrap (ncu: 55 % excessive wavefronts); pad the row to 8 tiles instead -- the extra
+    // lanes cost no time on these fetch-bound layers and store nothing
+    p.TPRR = w / 2;
+    p.TPR = (p.TPRR % 2) ? (int)align_up(p.TPRR, 8) : p.TPRR;
+    p.TPI = p.TPR * h;
     p.BW = 16;
     while (p.TPR % p.BW) p.BW >>= 1;
     // warps per CTA: the register file shared by one CTA (~2*KT accumulator registers +
     // patch/addressing); flags bits 8-15 cap it
     int wmax = std::min(20, 65536 / (32 * (2 * p.KT + 36)));
     if ((flags >> 8) & 0xff) wmax = std::min(wmax, (flags >> 8) & 0xff);
+    // very shallow inputs (the first layer, c = 3): the code is a few hundred
+    // instructions and each CTA mostly waits for its one TMA stage and stores -- several
+    // smaller CTAs per SM overlap those waits
+    if (c <= 16) wmax = std::min(wmax, 8);
     wmax = std::max(wmax, 1);
     const int cap = 32 * wmax;
     const int unit = 2 * p.BW;  // part boundaries keep pooling partners (lane ^ BW) together
@@ -234,7 +245,7 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     // row pitch: >= w + 2 (memory columns 0..w+1 of the halo layout), 16-byte multiple
     // (TMA box width); with BW < 16 a half-warp covers both rows of a row pair, whose
     // 8-byte patch loads stay on distinct banks when pitch/2 == 8 (mod 16)
-    p.P = (int)align_up(w + 2, 4);
+    p.P = (int)align_up(2 * p.TPR + 2, 4);
     if (p.BW < 16)
         while (p.P % 32 != 16) p.P += 4;
     if (p.P > 256) {
@@ -260,6 +271,7 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         --p.S;
     }
     p.CC = std::min(p.CC, c);
+    p.S = std::min<int>(p.S, (c + p.CC - 1) / p.CC);  // no stages beyond the chunks
     p.box_bytes = align_up((int64_t)p.CC * per_ch, 128);
     p.stage_bytes = p.NB * p.box_bytes;
     p.smem_bytes = p.S * p.stage_bytes + 8 * p.S;
@@ -375,6 +387,10 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
     o("shl.b32 row, r2, 1;");
     o("add.u32 row, row, par;");
     o("setp.eq.u32 pp0, par, 0;");
+    if (p.TPR != p.TPRR) {  // padded tile row: the columns past the image store nothing
+        o("setp.lt.u32 pl, col, %d;", p.TPRR);
+        o("and.pred pv, pv, pl;");
+    }
     o("sub.u32 bi, img, i0;");
     // smem row of the patch's first row (image row - 1): the first box starts at row
     // 2*ulo - 1, later boxes at -1
@@ -650,9 +666,15 @@ struct fscnn_sfjit {
     fscnn::Plan plan;
     // side streams + events for the concurrent group launches (created at first launch,
     // on the launching device)
-    std::vector<cudaStream_t> streams;
-    std::vector<cudaEvent_t> done;
-    cudaEvent_t fork = nullptr;
+    // per caller stream: that stream's own side streams + events (callers on different
+    // streams -- the engine's batch parts -- must not share side streams, or their group
+    // launches would serialise behind each other, in a captured graph too)
+    struct Side {
+        std::vector<cudaStream_t> streams;
+        std::vector<cudaEvent_t> done;
+        cudaEvent_t fork = nullptr;
+    };
+    std::vector<std::pair<cudaStream_t, Side>> sides;
     // the last input's tensor map (encoding one costs ~1 us of host time per launch)
     const float *map_x = nullptr;
     int map_n = 0, map_ldi = 0;
@@ -828,12 +850,19 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
         return FSCNN_OK;
     }
     const int n_side = (int)std::min<size_t>(j->groups.size(), 16);
-    if (n_side > 1 && (int)j->streams.size() < n_side) {
-        if (!j->fork && cudaEventCreateWithFlags(&j->fork, cudaEventDisableTiming) != cudaSuccess) {
+    fscnn_sfjit::Side *sd = nullptr;
+    for (auto &e : j->sides)
+        if (e.first == cs) sd = &e.second;
+    if (!sd) {
+        j->sides.emplace_back(cs, fscnn_sfjit::Side());
+        sd = &j->sides.back().second;
+    }
+    if (n_side > 1 && (int)sd->streams.size() < n_side) {
+        if (!sd->fork && cudaEventCreateWithFlags(&sd->fork, cudaEventDisableTiming) != cudaSuccess) {
             set_error("sfjit: event creation failed");
             return FSCNN_ERR_CUDA;
         }
-        while ((int)j->streams.size() < n_side) {
+        while ((int)sd->streams.size() < n_side) {
             cudaStream_t s2;
             cudaEvent_t e2;
             // highest priority: the groups of a layer go before other queued work
@@ -844,13 +873,13 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
                 set_error("sfjit: stream creation failed");
                 return FSCNN_ERR_CUDA;
             }
-            j->streams.push_back(s2);
-            j->done.push_back(e2);
+            sd->streams.push_back(s2);
+            sd->done.push_back(e2);
         }
     }
     if (n_side > 1) {
-        cudaEventRecord(j->fork, cs);
-        for (int i = 0; i < n_side; ++i) cudaStreamWaitEvent(j->streams[i], j->fork, 0);
+        cudaEventRecord(sd->fork, cs);
+        for (int i = 0; i < n_side; ++i) cudaStreamWaitEvent(sd->streams[i], sd->fork, 0);
     }
     // FSCNN_SFJIT_DEBUG=d > 0 (wrong results): launch g runs group g % d's code --
     // isolates the cost of the per-layer code footprint
@@ -858,7 +887,7 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
     for (size_t g = 0; g < j->groups.size(); ++g) {
         float *yg = y;  // each group's kernel offsets by its first filter itself
         void *args[] = {&map, &yg, &ldo_u, &nt_u};
-        cudaStream_t sg = n_side > 1 ? j->streams[g % n_side] : cs;
+        cudaStream_t sg = n_side > 1 ? sd->streams[g % n_side] : cs;
         r = d.launchKernel(j->groups[dbg > 0 ? g % dbg : g].fn, grid, 1, 1, (unsigned)p.T, 1, 1, (unsigned)p.smem_bytes,
                            reinterpret_cast<CUstream>(sg), args, nullptr);
         if (r != CUDA_SUCCESS) {
@@ -869,8 +898,8 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
     }
     if (n_side > 1) {
         for (int i = 0; i < n_side; ++i) {
-            cudaEventRecord(j->done[i], j->streams[i]);
-            cudaStreamWaitEvent(cs, j->done[i], 0);
+            cudaEventRecord(sd->done[i], sd->streams[i]);
+            cudaStreamWaitEvent(cs, sd->done[i], 0);
         }
     }
     return FSCNN_OK;
@@ -927,9 +956,11 @@ void fscnn_sfjit_destroy(fscnn_sfjit *j) {
     }
     for (auto &G : j->groups)
         if (G.mod && driver().moduleUnload) driver().moduleUnload(G.mod);
-    for (auto s2 : j->streams) cudaStreamDestroy(s2);
-    for (auto e2 : j->done) cudaEventDestroy(e2);
-    if (j->fork) cudaEventDestroy(j->fork);
+    for (auto &e : j->sides) {
+        for (auto s2 : e.second.streams) cudaStreamDestroy(s2);
+        for (auto e2 : e.second.done) cudaEventDestroy(e2);
+        if (e.second.fork) cudaEventDestroy(e.second.fork);
+    }
     delete j;
 }
 

@@ -127,8 +127,9 @@ class VGGEngine:
         # specialised kernels already spread each layer over concurrent per-group launches
         # batch split over concurrent streams: with the specialised kernels a layer's code
         # is fetched from HBM by the first part and found in L2 by the others, and one
-        # part's partial last wave overlaps another's next layer (VGG16 @224, batch 32:
-        # 4.7 -> 4.1 ms with 4 parts, replayed as a graph; tools/stack_probe.py)
+        # part's partial last wave overlaps another's next layer (VGG16 @224, batch 32,
+        # replayed as a graph: 1 part 4.79 ms, 2: 4.08, 4: 3.74, 8: 3.70;
+        # tools/stack_probe.py)
         self._jit_all = all(st.jit is not None for st in self.steps)
         self.use_graphs = os.environ.get("FSCNN_GRAPHS", "1") != "0"
         self._graphs = {}
@@ -171,7 +172,9 @@ class VGGEngine:
     def parts_for(self, n: int) -> int:
         if os.environ.get("FSCNN_PARTS"):
             return int(os.environ["FSCNN_PARTS"])
-        return 4 if self._jit_all and n >= SFJIT_MIN_BATCH else 2
+        if not (self._jit_all and n >= SFJIT_MIN_BATCH):
+            return 2
+        return 8 if n >= 64 else 4
 
     def _run(self, first: int, xin: torch.Tensor, parts: int) -> torch.Tensor:
         """_run_from through a CUDA graph captured once per (batch, entry layer, buffer):
@@ -253,12 +256,47 @@ class VGGEngine:
         lo..hi-1 into ``h_src`` just before their half is copied (host packing of the
         second half then overlaps the first half's copy and conv).
         """
-        bufs = self._buffers(n)
+        self._buffers(n)
         elems = self.in_c * self.hw * self.hw
         if getattr(self, "_d_in_n", None) != n:
             self._d_in = torch.empty(n * elems, dtype=torch.float32, device=self._in.device)
             self._d_in_n = n
             self._copy_stream = torch.cuda.Stream(device=self._in.device)
+        if not self.use_graphs:
+            return self._from_host_body(h_src, n, fill, graphed_tail=False)
+        # the whole device side -- part-wise H2D, layout conversion, the stack, the output
+        # conversion -- replayed as one CUDA graph per (batch, pinned source); host packing
+        # of pageable inputs happens first (it cannot be captured)
+        if fill is not None:
+            fill(0, n)
+        key = ("host", n, h_src.data_ptr())
+        entry = self._graphs.get(key)
+        if entry is None:
+            from . import _lib
+
+            cur = torch.cuda.current_stream()
+            self._from_host_body(h_src, n, None, graphed_tail=False)  # eager warm-up
+            side = torch.cuda.Stream(device=self._in.device)
+            side.wait_stream(cur)
+            g = torch.cuda.CUDAGraph()
+            n0 = _lib.launch_count()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    out = self._from_host_body(h_src, n, None, graphed_tail=False)
+            kernels = _lib.launch_count() - n0
+            _lib.load().fscnn_add_launch_count(-kernels)
+            cur.wait_stream(side)
+            entry = self._graphs[key] = (g, kernels, out)
+        g, kernels, out = entry
+        g.replay()
+        from . import _lib
+
+        _lib.load().fscnn_add_launch_count(kernels)
+        return out
+
+    def _from_host_body(self, h_src: torch.Tensor, n: int, fill, graphed_tail: bool) -> torch.Tensor:
+        bufs = self._buffers(n)
+        elems = self.in_c * self.hw * self.hw
         cur = torch.cuda.current_stream()
         cp = self._copy_stream
         cp.wait_stream(cur)  # the previous call's readers of _d_in are done
@@ -277,7 +315,9 @@ class VGGEngine:
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
             first.conv(self._in[lo:hi], bufs[0][lo:hi], self.hw, n)
-        return device.halo_to_whc(self._run(1, bufs[0], self.parts_for(n)), self.out_hw)
+        tail = self._run(1, bufs[0], self.parts_for(n)) if graphed_tail else \
+            self._run_from(1, bufs[0], self.parts_for(n))
+        return device.halo_to_whc(tail, self.out_hw)
 
     def run_exact(self, x: torch.Tensor) -> torch.Tensor:
         """Dense [N, C, H, W] -> [N, C', H', W'] through the reference-order kernels:

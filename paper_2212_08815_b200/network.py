@@ -21,8 +21,8 @@ from __future__ import annotations
 
 import math
 import struct
+import collections
 import threading
-import weakref
 import time
 from dataclasses import dataclass, replace
 
@@ -309,9 +309,10 @@ class _Staging:
 
     def __init__(self):
         self.key = None
-        # pinned_batch buffers by base address, held weakly: a buffer stays registered
-        # only while its DenseTensor3 views (or the caller) keep it alive
-        self.owned = weakref.WeakValueDictionary()
+        # pinned_batch buffers by base address, the most recent _OWNED_MAX of them (an LRU:
+        # the registry never grows without bound; an evicted batch still works, it is
+        # packed into the staging buffer like any pageable batch)
+        self.owned: "collections.OrderedDict[int, object]" = collections.OrderedDict()
 
     def get(self, n, in_elems, out_elems):
         import torch
@@ -330,10 +331,17 @@ class _Staging:
         tensor = self.owned.get(addr[0])
         if tensor is not None and len(batch) * nbytes <= tensor.numel() * 4 and all(
                 a == addr[0] + i * nbytes for i, a in enumerate(addr)):
+            self.owned.move_to_end(addr[0])
             return tensor[: len(batch) * elems]
         return None
 
+    def register(self, buf) -> None:
+        self.owned[buf.data_ptr()] = buf
+        while len(self.owned) > _OWNED_MAX:
+            self.owned.popitem(last=False)
 
+
+_OWNED_MAX = 16
 _staging = _Staging()
 # forward() may be called from several host threads (the reference's kernels are nogil
 # and its API thread-safe); the engine's device buffers and the pinned staging above are
@@ -351,9 +359,7 @@ def pinned_batch(n: int, dims) -> list:
     c, h, w = dims
     elems = c * h * w
     buf = torch.zeros(n * elems, dtype=torch.float32).pin_memory()
-    _staging.owned[buf.data_ptr()] = buf
-    # the numpy views keep the pinned tensor alive (base chain), so the weak registry
-    # entry lives exactly as long as the returned batch
+    _staging.register(buf)
     arr = buf.numpy().reshape(n, elems)
     return [DenseTensor3((c, h, w), arr[i]) for i in range(n)]
 

@@ -276,6 +276,7 @@ def test_pinned_batch_forward_equals_pageable():
     for t, a in zip(pinned, arrs):
         t.data[:] = fs.DenseTensor3.from_array(a).data
     ref = [o.data.tobytes() for o in fs.forward(prepared, pageable).outputs]
+    assert nw._staging.pinned_source(pinned, 3 * 32 * 32) is not None  # zero-copy path recognised
     assert [o.data.tobytes() for o in fs.forward(prepared, pinned).outputs] == ref
     assert [o.data.tobytes() for o in fs.forward(prepared, pinned[:3]).outputs] == ref[:3]
     rev = pinned[::-1]  # not back to back in memory -> packed path, same results

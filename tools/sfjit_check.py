@@ -39,7 +39,8 @@ def main():
              (64, 32, 224, 1, True, False)]
     cases = [cs + (0.9, 0, 0) for cs in cases] + [
         (64, 64, 56, 1, False, False, 0.95, 0, 8 | (1 << 16)), (24, 40, 12, 3, True, True, 0.9, 0, 4 | (1 << 16)),
-        (16, 72, 28, 2, True, False, 0.8, 0, 16 | (8 << 8) | (1 << 16))]
+        (16, 72, 28, 2, True, False, 0.8, 0, 16 | (8 << 8) | (1 << 16)),
+        (32, 64, 14, 5, True, True, 0.9, 0, 0), (16, 48, 6, 7, True, True, 0.9, 0, 0), (3, 64, 30, 3, True, True, 0.5, 0, 0)]
     ok = True
     for cs in cases:
         same, dt, info, (ref, got) = run_pair(*cs)
