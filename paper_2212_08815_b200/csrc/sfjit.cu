@@ -171,6 +171,7 @@ struct Plan {
     int odd_mode;  // kw = 1 pair: 0 = two 4-byte loads, 1 = moves from the even pairs
     int tma_hint;  // 1: input boxes loaded L2 evict-first
     int store_cs;  // 1: outputs stored streaming (evict-first)
+    int nobar;     // 1: per-stage empty mbarriers instead of a CTA barrier per chunk
 };
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -202,6 +203,7 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     p.odd_mode = getenv("FSCNN_SFJIT_ODD") ? atoi(getenv("FSCNN_SFJIT_ODD")) : 0;
     p.tma_hint = getenv("FSCNN_SFJIT_TMA_HINT") ? atoi(getenv("FSCNN_SFJIT_TMA_HINT")) : 1;
     p.store_cs = getenv("FSCNN_SFJIT_STORE_CS") ? atoi(getenv("FSCNN_SFJIT_STORE_CS")) : 1;
+    p.nobar = getenv("FSCNN_SFJIT_NOBAR") ? atoi(getenv("FSCNN_SFJIT_NOBAR")) : 1;
     // 48 filters per group: measured best on the VGG16 stack (32: -6 %, 64: -20 %; more
     // filters per group = less code per FMA, fewer warps per CTA sharing its fetch)
     p.KT = std::min(48, k);
@@ -218,7 +220,8 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     while (p.TPR % p.BW) p.BW >>= 1;
     // warps per CTA: the register file shared by one CTA (~2*KT accumulator registers +
     // patch/addressing); flags bits 8-15 cap it
-    int wmax = std::min(20, 65536 / (32 * (2 * p.KT + 36)));
+    const int wcap = getenv("FSCNN_SFJIT_WMAX") ? atoi(getenv("FSCNN_SFJIT_WMAX")) : 20;
+    int wmax = std::min(wcap, 65536 / (32 * (2 * p.KT + 36)));
     if ((flags >> 8) & 0xff) wmax = std::min(wmax, (flags >> 8) & 0xff);
     // very shallow inputs (the first layer, c = 3): the code is a few hundred
     // instructions and each CTA mostly waits for its one TMA stage and stores -- several
@@ -274,7 +277,7 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     p.S = std::min<int>(p.S, (c + p.CC - 1) / p.CC);  // no stages beyond the chunks
     p.box_bytes = align_up((int64_t)p.CC * per_ch, 128);
     p.stage_bytes = p.NB * p.box_bytes;
-    p.smem_bytes = p.S * p.stage_bytes + 8 * p.S;
+    p.smem_bytes = p.S * p.stage_bytes + 16 * p.S;  // full[S] + empty[S] mbarriers
     if (p.smem_bytes > 227 * 1024) {
         snprintf(why, why_n, "shared memory %lld bytes exceeds the limit", (long long)p.smem_bytes);
         return false;
@@ -412,6 +415,8 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
     o("createpolicy.fractional.L2::evict_first.b64 pol, 1.0;");
     o("@!pt0 bra PRO_DONE;");
     for (int s = 0; s < p.S; ++s) o("mbarrier.init.shared::cta.b64 [rbar+%d], 1;", 8 * s);
+    if (p.nobar)  // empty[s]: one arrival per warp when it is done reading stage s
+        for (int s = 0; s < p.S; ++s) o("mbarrier.init.shared::cta.b64 [rbar+%d], %d;", 8 * (p.S + s), p.WARPS);
     o("fence.mbarrier_init.release.cluster;");
     o("prefetch.tensormap [tm];");
     std::string lp = "p_";  // label prefix: prologue, then one per group
@@ -534,11 +539,25 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
             }
         }
         if (j + p.S < p.n_chunks) {
-            // every warp is done with stage s: thread 0 restages it with chunk j+S
-            o("barrier.sync 0;");
-            o("@!pt0 bra %sRS%d;", lp.c_str(), j);
-            issue(j + p.S);
-            o("%sRS%d:", lp.c_str(), j);
+            if (!p.nobar) {
+                // every warp is done with stage s: thread 0 restages it with chunk j+S
+                o("barrier.sync 0;");
+                o("@!pt0 bra %sRS%d;", lp.c_str(), j);
+                issue(j + p.S);
+                o("%sRS%d:", lp.c_str(), j);
+            } else {
+                // no CTA barrier: each warp arrives on empty[s]; thread 0 waits for all of
+                // them before restaging, the other warps run on (up to S-1 chunks ahead)
+                o("{ .reg .b32 ln; .reg .pred pz; and.b32 ln, tid, 31; setp.eq.u32 pz, ln, 0;");
+                o("@pz mbarrier.arrive.shared::cta.b64 _, [rbar+%d]; }", 8 * (p.S + s));
+                o("@!pt0 bra %sRS%d;", lp.c_str(), j);
+                o("mov.u32 q4, %d;", (j / p.S) & 1);
+                o("%sEW%d:", lp.c_str(), j);
+                o("mbarrier.try_wait.parity.shared::cta.b64 pw, [rbar+%d], q4;", 8 * (p.S + s));
+                o("@!pw bra %sEW%d;", lp.c_str(), j);
+                issue(j + p.S);
+                o("%sRS%d:", lp.c_str(), j);
+            }
         }
     }
 
