@@ -260,7 +260,8 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         snprintf(why, why_n, "box height %d exceeds the TMA limit", p.BH);
         return false;
     }
-    const int64_t budget = 215 * 1024;
+    // one CTA per SM by default; FSCNN_SFJIT_SMEM_KB (with FSCNN_SFJIT_MINB) packs more
+    const int64_t budget = (getenv("FSCNN_SFJIT_SMEM_KB") ? atoi(getenv("FSCNN_SFJIT_SMEM_KB")) : 215) * 1024;
     const int64_t per_ch = (int64_t)p.BH * p.P * 4;
     p.S = 4;
     for (;;) {
@@ -328,7 +329,7 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
     o(".extern .shared .align 1024 .b8 smem[];");
     o(".visible .entry sfjit(.param .align 64 .b8 tmap[128], .param .u64 py, .param .u32 pldo, .param .u32 pn)");
     o(".maxntid %d, 1, 1", p.T);
-    o(".minnctapersm 1");
+    o(".minnctapersm %d", getenv("FSCNN_SFJIT_MINB") ? atoi(getenv("FSCNN_SFJIT_MINB")) : 1);
     o("{");
     o(".reg .pred pv, pt0, pw, pl, pp0;");
     o(".reg .b32 tid, cta, nimg, i0, ulo, tt, img, r2, qq, par, col, row, bi, rb, ldo, nbox, y0f;");

@@ -9,23 +9,34 @@
 // Why a second kernel: the reference order pins every output's running sum to one
 // tap-major walk, so the exact kernels fetch a weight line per (node, output row) and
 // are bound by that weight stream (16 B of weights per 3 FMAs per lane).  Here the
-// order is free, so each weight is loaded once per (CTA, channel) into registers and
-// reused for every nonzero input of that channel in the tile:
-//   * a warp owns a 4 x 8 output tile of one image and 32*KT filters (lane = filter;
-//     KT = 2 from K = 128 up: the accumulator of an output is the register pair of two
-//     filters and every FMA an FFMA2 with the input value broadcast); a CTA's NW warps
-//     cover up to 512 filters of the same tile.
-//   * per 32-channel chunk the CTA decodes the 6 x 10 input region's node fibers into
-//     shared memory: values [32][region] plus, per channel, a bitmap of the region
-//     positions holding a node (each fiber read as one coalesced 32-node warp load,
-//     cursors kept across chunks; 8-warp CTAs prefetch the next chunk's windows with
-//     cp.async), then compacts the bitmaps into per-channel entry lists {pos, value}.
-//   * each warp walks the chunk's live channels (ascending) and, per channel, its
-//     entries (positions ascending): one jump-table branch per entry selects a block of
-//     <= 9 FMAs with compile-time accumulator and weight registers (si3x3_cases.inc).
-//     The next channel's weights are fetched while the current channel is applied.
-// No global atomics; the summation order is fixed, so results are deterministic and
-// independent of the batch, KT and the CTA size.
+// order is free, so each weight is loaded once per (warp, channel) into registers and
+// reused for every nonzero input of that channel in the warp's output tile.
+//
+// K >= 64 (two passes, si_tile_lists_kernel then si3x3_tl_kernel):
+//   1. tile streams: one warp per output tile merges its input region's node fibers (the
+//      reference's per-position channel lists) into ONE stream per tile: for every
+//      channel with a nonzero in the region (ascending), its entries {region position,
+//      value} in ascending position, closed by a link {NP, next channel}.  Count pass +
+//      warp scan + placement pass over the fibers; slots handed out by one atomic per
+//      tile (placement varies run to run, contents do not).
+//   2. conv: a warp owns one tile and 32*KT filters: KT = 2 (4 x 8 tiles, K < 128) or 4
+//      (4 x 4 tiles): the accumulator of an output is KT/2 register pairs (f, f') and
+//      every FMA an FFMA2 with the input value broadcast.  Its CTA's warps own
+//      consecutive tiles of the same filters, so the per-channel weight lines they load
+//      (9 x KT x 128 bytes) are mostly L1 hits.  The warp streams its tile's entries
+//      through a two-page shared ring with cp.async one page ahead and walks them with
+//      one jump-table branch per entry into a block of <= 9 x KT/2 FFMA2 with
+//      compile-time registers (si3x3_cases.inc).  No CTA barriers: warps are
+//      independent.  Measured bound (ncu, VGG16 layer 8, 90 % input zeros): the
+//      indirect branch rate (~1 per 14-18 cycles per SM whatever the tile shape or
+//      occupancy: 4x4/4x6/4x8 tiles at 16-32 warps/SM all ran within 10 %) and the
+//      weight stream (L1 60 % busy, 57 % hit); FMAs per branch is the lever (KT 2 -> 4:
+//      -20 % time).
+// K < 64 keeps the single-pass kernel below (one filter per lane, the region decoded per
+// 32-channel chunk in shared memory by the CTA).
+// No global atomics on the arithmetic; the summation order per output is fixed
+// (channels ascending, then region positions ascending), so results are deterministic
+// and independent of the batch, the tile placement and the stream layout.
 #include <algorithm>
 #include <stdlib.h>
 
@@ -40,9 +51,8 @@ constexpr int kSiCC = 32;  // channels per shared-memory chunk
 
 template <int KT> struct SiAcc;
 template <> struct SiAcc<1> { using T = float; };
-template <> struct SiAcc<2> { using T = unsigned long long; };  // (filter f0, filter f1)
 
-// KT filters per lane (lane l of warp w owns filters (w*KT + j)*32 + l, j < KT).
+// K < 64: one filter per lane (lane l of warp w owns filter w*32 + l).
 template <int TY, int TX, int NW, int KT>
 __global__ void __launch_bounds__(NW * 32, (TY * TX * KT <= 48 ? 24 : 16) / NW)
     si3x3_fast_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off,
@@ -172,10 +182,7 @@ __global__ void __launch_bounds__(NW * 32, (TY * TX * KT <= 48 ? 24 : 16) / NW)
 #pragma unroll
                 for (int t = 0; t < 9; ++t) wn[t] = __ldg(src + t * 32);
             }
-            if constexpr (KT == 1)
-                si_chan<TY, TX>(acc, wc, ents_base + 8u * (uint32_t)ch_off[c]);
-            else
-                si_chan2<TY, TX>(acc, wc, ents_base + 8u * (uint32_t)ch_off[c]);
+            si_chan<TY, TX>(acc, wc, ents_base + 8u * (uint32_t)ch_off[c]);
             if (cm == 0u) break;
             c = cn;
 #pragma unroll
@@ -254,19 +261,307 @@ __global__ void __launch_bounds__(NW * 32, (TY * TX * KT <= 48 ? 24 : 16) / NW)
     }
 }
 
-// Launch geometry for a layer of K filters; the bank layout depends on it.  KT filters
-// per lane, NW warps per CTA, and Kp = K padded with zero filters to whole CTAs (every
-// warp of the grid owns real bank rows).
+// Bank geometry for a layer of K filters: KT filters per lane and Kp = K padded with
+// zero filters.  K >= 64: two filters per lane in 64-filter warp groups (the two-pass
+// kernel); K < 64: one filter per lane, NW = 2 warps of the single-pass kernel.
 struct SiGeom {
     int kt, nw, kp;
 };
 inline SiGeom si_fast_geom(int k) {
     SiGeom g;
-    g.kt = k >= 128 ? 2 : 1;
-    const int groups = (int)ceil_div(k, 32 * g.kt);
-    g.nw = groups >= 8 ? 8 : (groups >= 4 ? 4 : 2);
-    g.kp = (int)ceil_div(k, 32 * g.kt * g.nw) * 32 * g.kt * g.nw;
+    if (k >= 64) {
+        g.kt = k >= 128 ? 4 : 2, g.nw = 0;
+        g.kp = (int)ceil_div(k, 32 * g.kt) * 32 * g.kt;
+    } else {
+        g.kt = 1, g.nw = 2;
+        g.kp = 64;
+    }
     return g;
+}
+
+// ---- K >= 64: tile streams + conv --------------------------------------------------
+
+constexpr int kPg = 256;  // entries per stream page (2 KB): the conv kernel's cp.async unit
+constexpr int kOvf = 64;  // ring overflow: a mirror of the head of the page in slot 0
+
+// Output tile TY x TX of one warp; its input region (TY + 2) x (TX + 2) has NP <= 64
+// positions; a channel block is <= NP entries + its link.
+template <int TY, int TX> struct SiTile {
+    static constexpr int RX = TX + 2, NP = (TY + 2) * RX, NA = TY * TX;
+    static_assert(NP < kOvf && TY % 2 == 0 && TX % 2 == 0, "tile");
+};
+
+// Pass 1: one warp per (tile, image), SI_LW tiles per CTA, no CTA barriers.  Stream =
+// head link {NP, first channel}, then per live channel (ascending) its entries {pos,
+// value} (positions ascending) and a link {NP, next channel or -1}.  Channels go in
+// blocks of SI_CB: pass A reads every region fiber (32-node coalesced windows, lane =
+// node) and counts nodes per channel (shared atomics: a fiber's channels are distinct);
+// a warp scan places the channel blocks; pass B re-reads the fibers in the same order
+// and writes each node at its block start + its rank (positions are visited in
+// ascending order, so the rank order is the position order).  Slots are handed out by
+// one atomic per tile (placement varies run to run, contents do not).
+constexpr int SI_LW = 4, SI_CB = 512;
+template <int TY, int TX>
+__global__ void __launch_bounds__(SI_LW * 32) si_tile_lists_kernel(
+    const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int64_t n_nodes, int n, int c_n, int h,
+    int w, int tiles_x, int tpi, unsigned long long *__restrict__ slot_ctr, int64_t cap_slots,
+    int64_t *__restrict__ tile_start, int2 *__restrict__ slots) {
+    constexpr int kNP = SiTile<TY, TX>::NP, kRX = SiTile<TY, TX>::RX;
+    __shared__ int cnt_s[SI_LW][SI_CB], st_s[SI_LW][SI_CB];
+    __shared__ int64_t qa_s[SI_LW][kNP], qe_s[SI_LW][kNP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x * SI_LW + warp, img = blockIdx.y;
+    if (tile >= tpi) return;
+    int(&cnt)[SI_CB] = cnt_s[warp];
+    int(&st)[SI_CB] = st_s[warp];
+    int64_t(&qa)[kNP] = qa_s[warp];
+    int64_t(&qe)[kNP] = qe_s[warp];
+    const int ty0 = (tile / tiles_x) * TY, tx0 = (tile % tiles_x) * TX;
+    const int64_t nseg = (int64_t)n * w * h;
+    int64_t nnz = 0;
+    for (int p = lane; p < kNP; p += 32) {
+        const int yy = ty0 - 1 + p / kRX, xx = tx0 - 1 + p % kRX;
+        int64_t q = 0, e = 0;
+        if (yy >= 0 && yy < h && xx >= 0 && xx < w) {
+            const int64_t i = ((int64_t)img * w + xx) * h + yy;
+            q = seg_off[i];
+            e = (i + 1 < nseg ? seg_off[i + 1] : n_nodes) - 1;  // the fiber's sentinel
+        }
+        qa[p] = q, qe[p] = e;
+        nnz += e - q;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) nnz += __shfl_xor_sync(0xffffffffu, nnz, d);
+    int64_t base = 0;
+    if (lane == 0) {
+        // entries + one link per live channel + the head link
+        const int64_t need = nnz + (nnz < c_n ? nnz : (int64_t)c_n) + 1;
+        base = (int64_t)atomicAdd(slot_ctr, (unsigned long long)need);
+        if (base + need > cap_slots) base = -1;  // cannot happen: cap_slots bounds the sum
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    tile_start[(int64_t)img * tpi + tile] = base;
+    if (base < 0) return;
+    int64_t out = base + 1;  // next free slot
+    int64_t link = base;     // the slot waiting for the next live channel
+    for (int cb0 = 0; cb0 < c_n; cb0 += SI_CB) {
+        const int cbn = min(SI_CB, c_n - cb0);
+        for (int i = lane; i < cbn; i += 32) cnt[i] = 0;
+        __syncwarp();
+        // pass A: count per channel
+        for (int p = 0; p < kNP; ++p) {
+            const int64_t e = qe[p];
+            for (int64_t q = qa[p]; q < e; q += 32) {
+                const int c = q + lane < e ? __ldg(&nodes[q + lane].x) - cb0 : SI_CB;
+                if (c < cbn) atomicAdd(&cnt[c], 1);
+                if (__any_sync(0xffffffffu, c >= cbn && q + lane < e)) break;  // rest in later blocks
+            }
+        }
+        __syncwarp();
+        // place the blocks: lane-strided groups of 32 channels, running offset
+        int64_t boff = 0;
+        for (int g0 = 0; g0 < cbn; g0 += 32) {
+            const int ci = g0 + lane;
+            const int k = ci < cbn ? cnt[ci] : 0;
+            const int size = k ? k + 1 : 0;
+            int inc = size;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += o;
+            }
+            const unsigned live = __ballot_sync(0xffffffffu, k > 0);
+            const int64_t start = out + boff + inc - size;
+            if (ci < cbn) st[ci] = (int)(boff + inc - size);
+            if (live) {
+                const int first = __ffs(live) - 1;
+                if (lane == 0) slots[link] = make_int2(kNP, cb0 + g0 + first);
+                const unsigned after = lane < 31 ? live & (0xfffffffeu << lane) : 0u;
+                if (k && after) slots[start + k] = make_int2(kNP, cb0 + g0 + __ffs(after) - 1);
+                link = __shfl_sync(0xffffffffu, start + k, 31 - __clz(live));
+            }
+            boff += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        for (int i = lane; i < cbn; i += 32) cnt[i] = 0;
+        __syncwarp();
+        // pass B: the same walk, every node to its block start + rank
+        for (int p = 0; p < kNP; ++p) {
+            const int64_t e = qe[p];
+            int64_t q = qa[p];
+            for (; q < e; q += 32) {
+                int2 nd = make_int2(SI_CB + cb0, 0);
+                if (q + lane < e) nd = __ldg(&nodes[q + lane]);
+                const int c = nd.x - cb0;
+                if (c < cbn) {
+                    const int rk = atomicAdd(&cnt[c], 1);
+                    slots[out + st[c] + rk] = make_int2(p, nd.y);
+                }
+                const unsigned beyond = __ballot_sync(0xffffffffu, c >= cbn && q + lane < e);
+                if (beyond) {  // the fiber continues in a later channel block
+                    q += __ffs(beyond) - 1;
+                    break;
+                }
+            }
+            if (lane == 0) qa[p] = q < e ? q : e;
+        }
+        out += boff;
+        __syncwarp();
+    }
+    if (lane == 0) slots[link] = make_int2(kNP, -1);
+}
+
+// Epilogue of the two-pass kernel: + bias (and Alg. 7's fused 2x2 pool, layers.py:345-390,
+// in pool2d's order -- (ph, pw) row-major, max from -inf with '>', avg as a left-to-right
+// sum (first NaN wins) / 4 -- before the bias), a zero sum stored as +0.0 (no node in
+// the reference).  Lane owns filters grp*64 + lane (low half) and grp*64 + 32 + lane.
+template <int kTY, int kTX, int PAIRS>
+__device__ __forceinline__ void si_store_pairs(const unsigned long long (&acc)[kTY * kTX * PAIRS], int grp, int lane,
+                                               int img, int ty0, int tx0, int h, int w, int k_n,
+                                               const float *__restrict__ bias, float *__restrict__ y, int pool) {
+#pragma unroll
+    for (int j = 0; j < 2 * PAIRS; ++j) {
+        const int k = (grp * 2 * PAIRS + j) * 32 + lane;
+        if (k >= k_n) continue;
+        const float bk = bias ? bias[k] : 0.0f;
+        if (pool) {
+            const int ho = h >> 1, wo = w >> 1;
+            float *yk = y + ((int64_t)img * k_n + k) * ho * wo;
+#pragma unroll
+            for (int qy = 0; qy < kTY / 2; ++qy) {
+                const int yy = (ty0 >> 1) + qy;
+                if (yy >= ho) break;
+#pragma unroll
+                for (int qx = 0; qx < kTX / 2; ++qx) {
+                    const int xx = (tx0 >> 1) + qx;
+                    if (xx >= wo) break;
+                    float m = pool == 1 ? -INFINITY : 0.0f;
+#pragma unroll
+                    for (int ph = 0; ph < 2; ++ph)
+#pragma unroll
+                        for (int pw = 0; pw < 2; ++pw) {
+                            const int o = (2 * qy + ph) * kTX + 2 * qx + pw;
+                            float v = __uint_as_float((unsigned)(acc[o * PAIRS + (j >> 1)] >> (32 * (j & 1))));
+                            v = (v != 0.0f) ? v : 0.0f;
+                            if (pool == 1) {
+                                if (v > m) m = v;
+                            } else if (!is_nan_bits(m)) {
+                                m = is_nan_bits(v) ? nan_quiet(v) : __fadd_rn(m, v);
+                            }
+                        }
+                    if (pool == 2 && !is_nan_bits(m)) m = __fdiv_rn(m, 4.0f);
+                    if (bias) m = __fadd_rn(m, bk);
+                    yk[(int64_t)yy * wo + xx] = m;
+                }
+            }
+        } else {
+            float *yk = y + ((int64_t)img * k_n + k) * h * w;
+#pragma unroll
+            for (int oy = 0; oy < kTY; ++oy) {
+                const int yy = ty0 + oy;
+                if (yy >= h) break;
+#pragma unroll
+                for (int ox = 0; ox < kTX; ++ox) {
+                    const int xx = tx0 + ox;
+                    if (xx >= w) break;
+                    float v = __uint_as_float((unsigned)(acc[(oy * kTX + ox) * PAIRS + (j >> 1)] >> (32 * (j & 1))));
+                    v = (v != 0.0f) ? v : 0.0f;
+                    if (bias) v = __fadd_rn(v, bk);
+                    yk[(int64_t)yy * w + xx] = v;
+                }
+            }
+        }
+    }
+}
+
+// Pass 2: NW warps per CTA, warp = (tile blockIdx.x*NW + warp, filter group blockIdx.y of
+// 64*PAIRS filters).  The tile's stream goes through a per-warp shared ring of two 2 KB
+// pages (absolute page q of the slot buffer in ring slot q & 1) plus an overflow area
+// that mirrors the head of the page in slot 0, so a channel block that runs off the end
+// of slot 1 reads on linearly; cp.async keeps the next page in flight, and before a block
+// that may reach the next page the warp waits for it.
+template <int TY, int TX, int PAIRS, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    si3x3_tl_kernel(const int2 *__restrict__ slots, const int64_t *__restrict__ tile_start, int n_tiles,
+                    int tiles_x, int tiles_per_img, int h, int w, const unsigned long long *__restrict__ wf,
+                    int k_n, int kp, const float *__restrict__ bias, float *__restrict__ y, int pool) {
+    constexpr int kTY = TY, kTX = TX, kNP = SiTile<TY, TX>::NP;
+    __shared__ __align__(16) int2 ring[NW][2 * kPg + kOvf];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * NW + warp;
+    if (t >= n_tiles) return;  // no CTA barriers below: warps are independent
+    const int grp = blockIdx.y;
+    const int img = t / tiles_per_img, r = t % tiles_per_img;
+    const int ty0 = (r / tiles_x) * kTY, tx0 = (r % tiles_x) * kTX;
+    unsigned long long acc[kTY * kTX * PAIRS];
+#pragma unroll
+    for (int i = 0; i < kTY * kTX * PAIRS; ++i) acc[i] = 0ull;
+    const int64_t s0 = tile_start[t];
+    if (s0 >= 0) {
+        const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(&ring[warp][0]);
+        // page q -> ring slot q & 1 (16 bytes per lane per copy); an even page's first
+        // kOvf entries also go to the overflow area behind slot 1
+        auto fetch = [&](int64_t q) {
+            const uint32_t dst = ring0 + (uint32_t)(q & 1) * (kPg * 8) + lane * 16;
+            const char *src = reinterpret_cast<const char *>(slots + q * kPg) + lane * 16;
+#pragma unroll
+            for (int i = 0; i < kPg * 8 / 512; ++i)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + i * 512), "l"(src + i * 512)
+                             : "memory");
+            if (!(q & 1))
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring0 + 2 * kPg * 8 + lane * 16),
+                             "l"(src)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        int64_t pg = s0 / kPg;  // page of the cursor; pages pg and pg + 1 are issued
+        fetch(pg);
+        fetch(pg + 1);  // the buffer has a spare page past the last slot handed out
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        bool next_ready = true;  // page pg + 1 has landed
+        int64_t pos = s0;        // absolute slot of the cursor
+        uint32_t cur = ring0 + (uint32_t)(pos & (2 * kPg - 1)) * 8;
+        int lx, ly;
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lx), "=r"(ly) : "r"(cur) : "memory");
+        ++pos;
+        // bank [C][Kp/(64 PAIRS)][9][32] of PAIRS (f, f') pairs
+        const unsigned long long *wk = wf + ((int64_t)grp * 288 + lane) * PAIRS;
+        const int64_t ch_stride = (int64_t)(kp / (64 * PAIRS)) * 288 * PAIRS;
+        while (ly >= 0) {
+            if (pos / kPg != pg) {  // the cursor entered the next page: refill the slot it left
+                ++pg;
+                if (!next_ready) {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    __syncwarp();
+                }
+                fetch(pg + 1);
+                next_ready = false;
+            }
+            if (!next_ready && (pos + kNP) / kPg != pg) {  // this block may reach page pg + 1
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+                next_ready = true;
+            }
+            cur = ring0 + (uint32_t)(pos & (2 * kPg - 1)) * 8;
+            unsigned long long wc[9 * PAIRS];
+            const unsigned long long *src = wk + ly * ch_stride;
+            if constexpr (PAIRS == 2) {
+#pragma unroll
+                for (int i = 0; i < 9; ++i) {
+                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(src + i * 64));
+                    wc[2 * i] = v.x, wc[2 * i + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 9; ++i) wc[i] = __ldg(src + i * 32);
+            }
+            const uint32_t c_in = cur;
+            si_chanp<kTY, kTX, PAIRS>(acc, wc, cur, lx, ly);
+            pos += (cur - c_in) >> 3;
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    si_store_pairs<TY, TX, PAIRS>(acc, grp, lane, img, ty0, tx0, h, w, k_n, bias, y, pool);
 }
 
 // [K][C][3][3] -> [C][Kp/(32 KT)][9][32][KT] (tap = kh*3 + kw; zero past K)
@@ -297,6 +592,65 @@ int launch_fast(const int2 *nodes, const int64_t *seg_off, int64_t n_nodes, int 
                                                                 tiles_x, bias, y, pool);
     FSCNN_LAUNCH_CHECK("si3x3_fast_kernel");
     return FSCNN_OK;
+}
+
+// Workspace of the two-pass path: [slot counter][tile_start: n_tiles][pad][slots].  The
+// slot budget bounds sum over tiles of (region nnz + live channels + 1): every node lies
+// in <= 4 tile regions ((TY+2) x (TX+2) regions over TY x TX tiles), every tile has <= C
+// live channels; two spare pages cover the conv kernel's read-ahead.
+struct SiWs {
+    int64_t n_tiles, cap_slots, off_ts, off_slots, bytes;
+};
+template <int TY, int TX>
+inline SiWs si_ws(int n, int c, int h, int w, int64_t n_nodes) {
+    SiWs s;
+    s.n_tiles = (int64_t)n * ceil_div(w, TX) * ceil_div(h, TY);
+    const int64_t inreg = 4 * n_nodes;
+    s.cap_slots = inreg + std::min<int64_t>(s.n_tiles * c, inreg) + s.n_tiles;
+    s.off_ts = 256;
+    s.off_slots = (s.off_ts + 8 * s.n_tiles + 255) / 256 * 256;
+    s.bytes = s.off_slots + (ceil_div(s.cap_slots, kPg) + 2) * (int64_t)kPg * 8;
+    return s;
+}
+
+template <int TY, int TX, int PAIRS, int NW, int MINB>
+int launch_tl(const int2 *nodes, const int64_t *seg_off, int64_t n_nodes, int n, int c, int h, int w,
+              const float *wf, int k, int kp, const float *bias, float *y, cudaStream_t st, int pool) {
+    const SiWs s = si_ws<TY, TX>(n, c, h, w, n_nodes);
+    static bool pool_set = false;
+    if (!pool_set) {
+        // keep freed workspace in the stream-ordered pool (no OS round trip per call)
+        int dev = 0;
+        cudaMemPool_t mp;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set = true;
+    }
+    char *ws = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&ws), (size_t)s.bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("si3x3 fast: workspace of %lld bytes could not be allocated", (long long)s.bytes);
+        return FSCNN_ERR_CUDA;
+    }
+    cudaMemsetAsync(ws, 0, 8, st);
+    const int tiles_x = (int)ceil_div(w, TX), tpi = tiles_x * (int)ceil_div(h, TY);
+    auto *ctr = reinterpret_cast<unsigned long long *>(ws);
+    auto *ts = reinterpret_cast<int64_t *>(ws + s.off_ts);
+    auto *slots = reinterpret_cast<int2 *>(ws + s.off_slots);
+    si_tile_lists_kernel<TY, TX><<<dim3((unsigned)ceil_div(tpi, SI_LW), (unsigned)n), SI_LW * 32, 0, st>>>(
+        nodes, seg_off, n_nodes, n, c, h, w, tiles_x, tpi, ctr, s.cap_slots, ts, slots);
+    int rc = check_launch("si_tile_lists_kernel");
+    if (rc == FSCNN_OK) {
+        dim3 grid((unsigned)ceil_div(s.n_tiles, NW), (unsigned)(kp / (64 * PAIRS)));
+        si3x3_tl_kernel<TY, TX, PAIRS, NW, MINB><<<grid, NW * 32, 0, st>>>(
+            slots, ts, (int)s.n_tiles, tiles_x, tpi, h, w, reinterpret_cast<const unsigned long long *>(wf), k,
+            kp, bias, y, pool);
+        rc = check_launch("si3x3_tl_kernel");
+    }
+    cudaFreeAsync(ws, st);
+    return rc;
 }
 
 }  // namespace
@@ -331,18 +685,17 @@ int fscnn_si_conv3x3_fast_pool(const fscnn_node *in_nodes, const int64_t *in_seg
     FSCNN_REQUIRE(in_nodes && in_seg_off && wf && y, "null buffer");
     FSCNN_REQUIRE(n <= 65535, "batch too large for one launch (%d > 65535)", n);
     const SiGeom g = si_fast_geom(k);
-    const int kt = g.kt, nw = g.nw, kp = g.kp;
     const int2 *nd = reinterpret_cast<const int2 *>(in_nodes);
     cudaStream_t st = as_stream(stream);
-    if (kt == 2) {
-        if (nw == 8) return launch_fast<4, 8, 8, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
-        if (nw == 4) return launch_fast<4, 8, 4, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
-        return launch_fast<4, 8, 2, 2>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+    if (g.kt >= 2) {
+        FSCNN_REQUIRE(n * (int64_t)ceil_div(w, 4) * ceil_div(h, 4) < (1ll << 31), "too many tiles");
+        // 4 filters per lane on 4 x 4 tiles from K = 128 (twice the FMAs per jump-table
+        // branch of 2 filters on 4 x 8, the better trade once K fills 128-filter groups)
+        if (g.kt == 2) return launch_tl<4, 8, 1, 4, 5>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, g.kp, bias, y, st, pool);
+        return launch_tl<4, 4, 2, 4, 4>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, g.kp, bias, y, st, pool);
     }
-    // one filter per lane (K < 128)
-    if (nw == 8) return launch_fast<4, 8, 8, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
-    if (nw == 4) return launch_fast<4, 8, 4, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
-    return launch_fast<4, 8, 2, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, kp, bias, y, st, pool);
+    // one filter per lane (K < 64)
+    return launch_fast<4, 8, 2, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, g.kp, bias, y, st, pool);
 }
 
 int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,

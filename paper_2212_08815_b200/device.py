@@ -478,7 +478,8 @@ def si_conv3x3(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: in
 
 def si_pack_fast(w_kc33: torch.Tensor) -> torch.Tensor:
     """Dense [K, C, 3, 3] bank -> the channel-major kernel's [C][Kp/(32 KT)][9][32][KT]
-    layout (KT = filters per lane: 2 for K >= 128, else 1; Kp = K rounded up to 32 KT)."""
+    layout (KT = filters per lane: 4 from K = 128, 2 from K = 64, else 1; Kp = K rounded
+    up to 32 KT, 64 at least)."""
     w = w_kc33.contiguous()
     k, c = int(w.shape[0]), int(w.shape[1])
     n = int(_lib.load().fscnn_si_fast_bank_floats(k, c))
@@ -487,21 +488,22 @@ def si_pack_fast(w_kc33: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def si_fast_ctas(n: int, h: int, w: int, k: int) -> int:
-    """CTAs the channel-major SI kernel launches (mirrors si_fast_geom in si_fast.cu)."""
-    kt = 2 if k >= 128 else 1
-    groups = -(-k // (32 * kt))
-    nw = 8 if groups >= 8 else (4 if groups >= 4 else 2)
-    return n * -(-h // 4) * -(-w // 8) * -(-k // (32 * kt * nw))
+def si_fast_warps(n: int, h: int, w: int, k: int) -> int:
+    """Warps of the two-pass channel-major SI kernel (K >= 64): one per (output tile,
+    filter group) -- 4x8 tiles x 64 filters below K = 128, 4x4 tiles x 128 filters from
+    there -- mirroring si3x3_tl_kernel's grid in si_fast.cu."""
+    if k < 128:
+        return n * -(-h // 4) * -(-w // 8) * -(-k // 64)
+    return n * -(-h // 4) * -(-w // 4) * -(-k // 128)
 
 
 def si_use_fast(h: int, w: int, k: int) -> bool:
     """The layer API's choice for a 3x3/s1/p1 sparse-input conv of one h x w image with k
-    filters: the channel-major kernel when one image already fills the GPU and the
-    filter count fills its 32-filter lane groups (K >= 64; below that most lanes of a
-    group would carry padding filters), else the bit-exact strip kernel.  Depends on the
-    image shape only, never on the batch, so batched and per-image runs agree bitwise."""
-    return k >= 64 and si_fast_ctas(1, h, w, k) >= 148
+    filters: the channel-major kernel when one image already gives every SM two warps
+    and the filter count fills its 64-filter lane pairs (K >= 64), else the bit-exact
+    strip kernel.  Depends on the image shape only, never on the batch, so batched and
+    per-image runs agree bitwise."""
+    return k >= 64 and si_fast_warps(1, h, w, k) >= 2 * 148
 
 
 def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,

@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--peak", type=float, default=72.3, help="FP32 TFLOP/s denominator (measured probe)")
     ap.add_argument("--hbm", type=float, default=None, help="HBM GB/s (default MEASURED_PEAKS.json)")
     ap.add_argument("--modes", default="sf,sf_jt,si,si_fast")
+    ap.add_argument("--zf", default=None, help="comma list restricting the zero fractions")
     args = ap.parse_args()
     if args.hbm is None:
         try:
@@ -94,13 +95,16 @@ def main():
         r["frac_of_fp32_peak"] = r["tflops"] / args.peak
         return r
 
+    def zfs(default):
+        return [float(v) for v in args.zf.split(",")] if args.zf else default
+
     shapes = wl.vgg16_conv_shapes()
     layers = [int(v) for v in args.layers.split(",")] if args.layers else range(len(shapes))
     rows = []
     for li in layers:
         c, k, h, w = shapes[li]
         modes = args.modes.split(",")
-        for zf in (0.5, 0.75, 0.9, 0.95, 0.99) if ("sf" in modes or "sf_jt" in modes) else ():
+        for zf in zfs((0.5, 0.75, 0.9, 0.95, 0.99)) if ("sf" in modes or "sf_jt" in modes) else ():
             x, wt, b = wl.sweep_layer(li, "sf", zf, n=args.n)
             wd = torch.from_numpy(wt).cuda()
             xh = device.to_halo(torch.from_numpy(x).cuda())
@@ -131,7 +135,7 @@ def main():
                 rows.append(roof(r, nbytes))
                 print(json.dumps(r), flush=True)
             del xh, out, enc, x2, ex
-        for zf in (0.5, 0.75, 0.9, 0.95) if ("si" in modes or "si_fast" in modes) else ():
+        for zf in zfs((0.5, 0.75, 0.9, 0.95)) if ("si" in modes or "si_fast" in modes) else ():
             x, wt, b = wl.sweep_layer(li, "si", zf, n=args.n)
             xd = torch.from_numpy(x).cuda()
             enc = device.encode_order(xd, "CHW")
