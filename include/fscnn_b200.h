@@ -211,14 +211,16 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
 /* 3x3 / stride 1 / pad 1 channel-major path (the same contraction as
  * _conv_input_sparse_kernel, kernels.py:136-166, summed channel by channel: results
  * within fp32 reassociation of the reference, north-star tolerance max|err| <=
- * 1e-4 max|ref|; deterministic).  A CTA owns a 4x8 output tile of one image and up to
- * 512 filters (KT = 2 filters per lane from K = 128 up, else 1); per 32-channel chunk it
- * decodes the tile's input region into shared memory, then each lane applies every
- * nonzero input of a channel with that channel's 9 weights (per filter) held in
- * registers.  wf: [c][Kp/(32 KT)][9][32][KT] floats (tap = kh*3+kw, Kp = K padded with
- * zero filters to whole CTAs), built by fscnn_si_pack_fast from a dense [K][C][3][3]
- * bank; fscnn_si_fast_bank_floats gives its size.  n_nodes: length of
- * in_nodes (bounds the 32-node fiber reads).  Replaces the same call as
+ * 1e-4 max|ref|; deterministic).  K >= 64: a pre-pass merges each output tile's input
+ * region fibers into one per-tile channel stream (workspace from the stream-ordered
+ * pool: cudaMallocAsync/cudaFreeAsync on `stream`, graph-capturable), then a warp per
+ * (tile, filter group) applies every nonzero of a channel with that channel's 9 weights
+ * (per filter) held in registers: KT = 4 filters per lane on 4x4 tiles from K = 128,
+ * KT = 2 on 4x8 tiles from K = 64; K < 64: one filter per lane, single pass.
+ * wf: [c][Kp/(32 KT)][9][32][KT] floats (tap = kh*3+kw, Kp = K padded with zero
+ * filters to a multiple of 32 KT, 64 at least), built by fscnn_si_pack_fast from a dense
+ * [K][C][3][3] bank; fscnn_si_fast_bank_floats gives its size.  n_nodes: length of
+ * in_nodes (bounds the fiber reads and sizes the workspace).  Replaces the same call as
  * fscnn_si_conv3x3 (layers.py:425-428 conv_forward_sparse_input). */
 int64_t fscnn_si_fast_bank_floats(int k, int c);
 int fscnn_si_pack_fast(const float *w_kc33, int k, int c, float *wf, void *stream);
