@@ -200,7 +200,11 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
         snprintf(why, why_n, "extents must be even (1x2 lane tiles, 2x2 pooling windows)");
         return false;
     }
-    p.odd_mode = getenv("FSCNN_SFJIT_ODD") ? atoi(getenv("FSCNN_SFJIT_ODD")) : 0;
+    // kw = 1 pair: two 4-byte loads (their half-warps collide on odd banks: 2 wavefronts
+    // each) or moves from the even pairs (more code).  Shared-memory-bound shallow layers
+    // (C <= 64: few channels, the code stays cached) take the moves: VGG16 L1 -10 %,
+    // L2 -5 %; the fetch-bound deep layers keep the loads (L3/L4 +3-7 % with moves)
+    p.odd_mode = getenv("FSCNN_SFJIT_ODD") ? atoi(getenv("FSCNN_SFJIT_ODD")) : (c > 16 && c <= 64 ? 1 : 0);
     p.tma_hint = getenv("FSCNN_SFJIT_TMA_HINT") ? atoi(getenv("FSCNN_SFJIT_TMA_HINT")) : 1;
     p.store_cs = getenv("FSCNN_SFJIT_STORE_CS") ? atoi(getenv("FSCNN_SFJIT_STORE_CS")) : 1;
     p.nobar = getenv("FSCNN_SFJIT_NOBAR") ? atoi(getenv("FSCNN_SFJIT_NOBAR")) : 1;
@@ -585,6 +589,8 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
     o("mul.wide.u32 ks, ldo, %d;", HO * 4);  // bytes between filter planes
     // pooled results are stored by the row-0 lane of each window
     if (p.pool) o("and.pred pv, pv, pp0;");
+    // (aligned 8-byte pair stores -- the left lane's f1 shuffled in -- measured slower on
+    // the store-bound first layer, 0.140 -> 0.157 ms, and neutral elsewhere)
     auto relu_np = [&](const char *f) {
         // keep v if its bits are > 0 as int (positive, not -0.0) or it is a NaN
         o("{ .reg .b32 u, m; .reg .pred k1, k2; mov.b32 u, %s; setp.gt.s32 k1, u, 0; and.b32 m, u, 2147483647; "
