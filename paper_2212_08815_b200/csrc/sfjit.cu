@@ -219,6 +219,13 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     // lanes cost no time on these fetch-bound layers and store nothing
     p.TPRR = w / 2;
     p.TPR = (p.TPRR % 2) ? (int)align_up(p.TPRR, 8) : p.TPRR;
+    // a 9..15-tile row (w = 28: 14 tiles) has BW = 2 and wraps a warp across row pairs:
+    // the second half-warp's 8-byte patch loads then collide on 8 of 32 banks (ncu: 44 %
+    // excessive wavefronts, the warm-code bound of these layers); padding the row to 16
+    // tiles (BW = 16, 12.5 % idle lanes) measured VGG16 L7 -16 %, L8 -18 %.  Wider rows
+    // (56 -> 64, 28 -> 32 tiles) measured neutral to slower and keep their width
+    if (p.TPRR > 8 && p.TPRR < 16) p.TPR = 16;
+    if (getenv("FSCNN_SFJIT_PADTPR")) p.TPR = (int)align_up(p.TPRR, atoi(getenv("FSCNN_SFJIT_PADTPR")));
     p.TPI = p.TPR * h;
     p.BW = 16;
     while (p.TPR % p.BW) p.BW >>= 1;
@@ -490,6 +497,13 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
         o("@pl trap;");
         o("bra.uni %sWT%d;", lp.c_str(), j);
         o("%sWD%d:", lp.c_str(), j);
+        // debug (FSCNN_SFJIT_REPEAT=R): run the chunk's code R times on the same stage
+        // (wrong results) -- measures the cost of a warm re-execution of the code
+        const int rep = getenv("FSCNN_SFJIT_REPEAT") ? atoi(getenv("FSCNN_SFJIT_REPEAT")) : 1;
+        if (rep > 1) {
+            o("mov.u32 q3, 0;");
+            o("%sRP%d:", lp.c_str(), j);
+        }
         const int cend = std::min(p.C, (j + 1) * p.CC);
         for (int c = j * p.CC; c < cend; ++c) {
             const int cl = c - j * p.CC;
@@ -542,6 +556,11 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
                 else
                     o("fma.rn.f32x2 a%d, e%d, dw, a%d;", z.kl, 2 * z.kh + z.kw / 2, z.kl);
             }
+        }
+        if (rep > 1) {
+            o("add.u32 q3, q3, 1;");
+            o("setp.lt.u32 pl, q3, %d;", rep);
+            o("@pl bra %sRP%d;", lp.c_str(), j);
         }
         if (j + p.S < p.n_chunks) {
             if (!p.nobar) {

@@ -314,7 +314,8 @@ def test_si_fast_within_tolerance(dev, oracle):
     rng = np.random.default_rng(41)
     cases = [(2, 37, 70, 13, 29, 0.8), (1, 5, 3, 1, 1, 0.5), (3, 64, 33, 28, 28, 0.9), (1, 130, 257, 9, 17, 0.95),
              (2, 16, 64, 8, 8, 0.0), (1, 40, 32, 10, 12, 1.0), (4, 96, 128, 14, 14, 0.5),
-             (1, 70, 200, 11, 9, 0.0), (2, 100, 160, 7, 13, 0.9)]
+             (1, 70, 200, 11, 9, 0.0), (2, 100, 160, 7, 13, 0.9), (2, 64, 300, 10, 14, 0.5),
+             (1, 33, 512, 6, 9, 0.9)]
     for (n, c, k, h, wd, zf) in cases:
         x = np.abs(rng.standard_normal((n, c, h, wd))).astype(np.float32)
         x[rng.random(x.shape) < zf] = 0
