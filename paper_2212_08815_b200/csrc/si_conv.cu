@@ -19,6 +19,33 @@ namespace {
 
 constexpr int kPixPerBlock = 8;  // warps per block, one output pixel each
 
+// Calls f(c, v) for the nodes of segment s in order (the reference's fiber walk).  The
+// segments are consecutive (seg_off[s + 1] = seg_off[s] + count + 1, the sentinel last),
+// so the fiber's length is known up front: the warp reads it 32 nodes per coalesced load
+// and broadcasts them, instead of a chain of dependent single-node loads (one L2 round
+// trip per node, the latency that bounds a one-image layer).  COOP = false keeps the
+// single-node walk: with a full GPU of warps the latency is hidden and the two shuffles
+// per node cost more (batch 32: 1.5-2x slower with COOP, measured).  The batch's last segment
+// has no successor offset and keeps the sentinel walk.  Warp-uniform: every lane calls f
+// for every node.
+template <bool COOP, typename F>
+__device__ __forceinline__ void walk_fiber(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off,
+                                           int64_t s, int64_t n_seg, int lane, F &&f) {
+    int64_t q = seg_off[s];
+    if (COOP && s + 1 < n_seg) {
+        const int64_t e = seg_off[s + 1] - 1;
+        for (; q < e; q += 32) {
+            const int cnt = (int)(e - q < 32 ? e - q : 32);
+            int2 mine = make_int2(0, 0);
+            if (lane < cnt) mine = nodes[q + lane];
+            for (int t = 0; t < cnt; ++t)
+                f(__shfl_sync(0xffffffffu, mine.x, t), __int_as_float(__shfl_sync(0xffffffffu, mine.y, t)));
+        }
+    } else {
+        for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) f(nd.x, __int_as_float(nd.y));
+    }
+}
+
 __global__ void __launch_bounds__(kPixPerBlock * 32)
     si_gather_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int c_n,
                      int h_i, int w_i, const float *__restrict__ wt, int k_n, int h_f, int w_f,
@@ -75,7 +102,7 @@ __global__ void __launch_bounds__(128, 8)
     const int img = blockIdx.z;
     const bool live = k < k_n;
     const int kq = live ? k : 0;
-    const int64_t *so = seg_off + (int64_t)img * h_i * w_i;
+    const int64_t seg0 = (int64_t)img * h_i * w_i, n_seg = (int64_t)gridDim.z * h_i * w_i;
     float acc[S];
 #pragma unroll
     for (int t = 0; t < S; ++t) acc[t] = 0.0f;
@@ -87,10 +114,8 @@ __global__ void __launch_bounds__(128, 8)
         for (int kk = 0; kk < 3; ++kk) {
             const int h_in = i - 1 + kk;
             if (h_in < 0 || h_in >= h_i) continue;
-            int64_t q = so[(int64_t)w_in * h_i + h_in];
-            for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) {
-                const float v = __int_as_float(nd.y);
-                const float4 wv = wq[((int64_t)nd.x * 3 + kk) * k_n + kq];
+            walk_fiber<false>(nodes, seg_off, seg0 + (int64_t)w_in * h_i + h_in, n_seg, lane, [&](int ch, float v) {
+                const float4 wv = wq[((int64_t)ch * 3 + kk) * k_n + kq];
                 // output j' = col - l (strip-relative), tap l = 0,1,2
 #pragma unroll
                 for (int l = 0; l < 3; ++l) {
@@ -99,7 +124,7 @@ __global__ void __launch_bounds__(128, 8)
                     const float w = l == 0 ? wv.x : (l == 1 ? wv.y : wv.z);
                     acc[jp] = __fadd_rn(acc[jp], __fmul_rn(w, v));
                 }
-            }
+            });
         }
     }
     if (!live) return;
@@ -118,7 +143,7 @@ __global__ void __launch_bounds__(128, 8)
 // [c][kh][32] float4 bank in shared memory (1.5 KB per channel) and walks many strips, so
 // every weight comes from shared memory; per-output order and arithmetic are the strip
 // kernel's (bit-exact).
-template <int S>
+template <int S, bool COOP>
 __global__ void __launch_bounds__(512)
     si_strip_smem_kernel(const int2 *__restrict__ nodes, const int64_t *__restrict__ seg_off, int n_img,
                          int c_n, int h_i, int w_i, const float4 *__restrict__ wq, int k_n, int strips,
@@ -127,20 +152,79 @@ __global__ void __launch_bounds__(512)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     const int k = blockIdx.y * 32 + lane;
     const bool live = k < k_n;
+    // stage the bank with cp.async (all of a thread's 16-byte copies in flight at once;
+    // filters past K zero-filled)
+    const uint32_t ws0 = (uint32_t)__cvta_generic_to_shared(ws);
     for (int idx = threadIdx.x; idx < c_n * 3 * 32; idx += blockDim.x) {
         const int row = idx >> 5, kk = blockIdx.y * 32 + (idx & 31);
-        ws[idx] = kk < k_n ? wq[(int64_t)row * k_n + kk] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 *src = wq + (int64_t)row * k_n + (kk < k_n ? kk : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ws0 + idx * 16), "l"(src),
+                     "r"(kk < k_n ? 16 : 0)
+                     : "memory");
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int64_t jobs = (int64_t)n_img * h_i * strips;
-    for (int64_t job = (int64_t)blockIdx.x * nwarp + warp; job < jobs; job += (int64_t)gridDim.x * nwarp) {
+    // one-image problems deal jobs round-robin over the CTAs (job = warp * grid + cta): a
+    // grid sized to the SMs then keeps every SM busy with fewer jobs than warps (config 2:
+    // 15 -> 13 us); large ones keep consecutive jobs (shared input rows) in a CTA
+    const int64_t j_first = COOP ? (int64_t)warp * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * nwarp + warp;
+    for (int64_t job = j_first; job < jobs; job += (int64_t)gridDim.x * nwarp) {
         const int img = (int)(job / ((int64_t)h_i * strips));
         const int rem = (int)(job % ((int64_t)h_i * strips));
         const int i = rem / strips, j0 = (rem % strips) * S;
-        const int64_t *so = seg_off + (int64_t)img * h_i * w_i;
+        const int64_t seg0 = (int64_t)img * h_i * w_i, n_seg = (int64_t)n_img * h_i * w_i;
         float acc[S];
 #pragma unroll
         for (int t = 0; t < S; ++t) acc[t] = 0.0f;
+        if constexpr (COOP && S <= 4) {
+            // one-image problems: issue every fiber's offsets, then every fiber's first 32
+            // nodes, before any arithmetic (two L2 round trips per job instead of two per
+            // fiber); then the reference-order walk over the registers
+            constexpr int NF = (S + 2) * 3;
+            int64_t fq[NF], fe[NF];
+            int2 fm[NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int w_in = j0 - 1 + f / 3, h_in = i - 1 + f % 3;
+                const bool ok = w_in >= 0 && w_in < w_i && h_in >= 0 && h_in < h_i;
+                const int64_t sg = seg0 + (int64_t)w_in * h_i + h_in;
+                fq[f] = ok ? seg_off[sg] : 0;
+                fe[f] = !ok ? 0 : (sg + 1 < n_seg ? seg_off[sg + 1] - 1 : -1);  // -1: walk to the sentinel
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int64_t cnt = fe[f] < 0 ? 0 : fe[f] - fq[f];
+                fm[f] = lane < cnt ? nodes[fq[f] + lane] : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int col = f / 3, kk = f % 3;
+                auto apply = [&](int ch, float v) {
+                    const float4 wv = ws[(ch * 3 + kk) * 32 + lane];
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) {
+                        const int jp = col - l;
+                        if (jp < 0 || jp >= S) continue;
+                        const float wl = l == 0 ? wv.x : (l == 1 ? wv.y : wv.z);
+                        acc[jp] = __fadd_rn(acc[jp], __fmul_rn(wl, v));
+                    }
+                };
+                if (fe[f] < 0) {
+                    int64_t q = fq[f];
+                    for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) apply(nd.x, __int_as_float(nd.y));
+                    continue;
+                }
+                int2 mine = fm[f];
+                for (int64_t q = fq[f]; q < fe[f]; q += 32) {
+                    const int cnt = (int)(fe[f] - q < 32 ? fe[f] - q : 32);
+                    if (q != fq[f]) mine = lane < cnt ? nodes[q + lane] : make_int2(0, 0);
+#pragma unroll 4
+                    for (int t = 0; t < cnt; ++t)
+                        apply(__shfl_sync(0xffffffffu, mine.x, t), __int_as_float(__shfl_sync(0xffffffffu, mine.y, t)));
+                }
+            }
+        } else {
 #pragma unroll
         for (int col = 0; col < S + 2; ++col) {
             const int w_in = j0 - 1 + col;
@@ -149,10 +233,8 @@ __global__ void __launch_bounds__(512)
             for (int kk = 0; kk < 3; ++kk) {
                 const int h_in = i - 1 + kk;
                 if (h_in < 0 || h_in >= h_i) continue;
-                int64_t q = so[(int64_t)w_in * h_i + h_in];
-                for (int2 nd = nodes[q]; nd.x != -1; nd = nodes[++q]) {
-                    const float v = __int_as_float(nd.y);
-                    const float4 wv = ws[(nd.x * 3 + kk) * 32 + lane];
+                walk_fiber<COOP>(nodes, seg_off, seg0 + (int64_t)w_in * h_i + h_in, n_seg, lane, [&](int ch, float v) {
+                    const float4 wv = ws[(ch * 3 + kk) * 32 + lane];
 #pragma unroll
                     for (int l = 0; l < 3; ++l) {
                         const int jp = col - l;
@@ -160,8 +242,9 @@ __global__ void __launch_bounds__(512)
                         const float wl = l == 0 ? wv.x : (l == 1 ? wv.y : wv.z);
                         acc[jp] = __fadd_rn(acc[jp], __fmul_rn(wl, v));
                     }
-                }
+                });
             }
+        }
         }
         if (!live) continue;
 #pragma unroll
@@ -228,8 +311,10 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
         // shallow bank: weights in shared memory, persistent CTAs (1 or 2 per SM)
         const int per_sm = ws_bytes <= 100 * 1024 ? 2 : 1;
         const int64_t jobs = (int64_t)n * h * strips;
+        // one-image problems: one CTA per SM over all filter blocks (jobs dealt
+        // round-robin), fewer when there are not ~4 jobs per CTA
         const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(ceil_div(148 * per_sm, k_blocks),
-                                                                    ceil_div(jobs, 16)));
+                                                                    ceil_div(jobs, small ? 4 : 16)));
         dim3 g2((unsigned)ctas, (unsigned)k_blocks, 1);
         auto launch = [&](auto kern) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws_bytes);
@@ -237,9 +322,17 @@ int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int 
                                                           n, c, h, w, reinterpret_cast<const float4 *>(wq), k,
                                                           strips, bias, y);
         };
-        if (S == 8) launch(si_strip_smem_kernel<8>);
-        else if (S == 4) launch(si_strip_smem_kernel<4>);
-        else launch(si_strip_smem_kernel<2>);
+        // one-image problems (config 2): the fiber walks' L2 latency is exposed, so read
+        // fibers 32 nodes per coalesced load (walk_fiber COOP)
+        if (small) {
+            if (S == 8) launch(si_strip_smem_kernel<8, true>);
+            else if (S == 4) launch(si_strip_smem_kernel<4, true>);
+            else launch(si_strip_smem_kernel<2, true>);
+        } else {
+            if (S == 8) launch(si_strip_smem_kernel<8, false>);
+            else if (S == 4) launch(si_strip_smem_kernel<4, false>);
+            else launch(si_strip_smem_kernel<2, false>);
+        }
         FSCNN_LAUNCH_CHECK("si_strip_smem_kernel");
         return FSCNN_OK;
     }
