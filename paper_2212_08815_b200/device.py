@@ -501,9 +501,13 @@ def si_use_fast(h: int, w: int, k: int) -> bool:
     """The layer API's choice for a 3x3/s1/p1 sparse-input conv of one h x w image with k
     filters: the channel-major kernel when one image already gives every SM two warps
     and the filter count fills its 64-filter lane pairs (K >= 64), else the bit-exact
-    strip kernel.  Depends on the image shape only, never on the batch, so batched and
-    per-image runs agree bitwise."""
-    return k >= 64 and si_fast_warps(1, h, w, k) >= 2 * 148
+    strip kernel.  Deep layers (K >= 256: VGG16's 512-filter 28x28 and 14x14 convs) take
+    the channel-major kernel from 64 warps per image: one image then runs 0.96-1.8x the
+    strip kernel's time, a batch of 32 3.7-4.3x faster (measured,
+    profiles/r02_si_rule_n1.txt).  Depends on the image shape only, never on the batch,
+    so batched and per-image runs agree bitwise."""
+    warps = si_fast_warps(1, h, w, k)
+    return k >= 64 and (warps >= 2 * 148 or (k >= 256 and warps >= 64))
 
 
 def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, h: int, w: int,

@@ -412,19 +412,78 @@ def _batched_inputs_ok(prepared: PreparedNet, batch) -> bool:
     """The batched device path covers all three variants for inputs the per-image path
     would accept unchanged (sparse_input: CHW node tensors without explicit zero-valued
     nodes -- the batch travels as dense device planes, where a stored zero and an absent
-    node coincide); anything else takes the per-image path and its validation."""
+    node coincide); anything else takes the per-image path and its validation.
+    (The zero-valued-node test runs on the device inside _forward_batched, which then
+    declines the batch.)"""
     variant = prepared.net.variant
     if not prepared.steps:
         return False
     if variant == VARIANT_SPARSE_INPUT:
-        for t in batch:
-            if t.order is not AxisOrder3.CHW:
-                return False
-            nodes = np.asarray(t.nodes)
-            live = nodes["index"] >= 0
-            if np.any(nodes["value"][live] == 0):
-                return False
+        return all(t.order is AxisOrder3.CHW for t in batch)
     return True
+
+
+_pinned_in: dict = {}  # grow-only pinned staging for the sparse-input batch upload
+
+
+def _pinned(key: str, nbytes: int):
+    import torch
+
+    buf = _pinned_in.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        _pinned_in[key] = buf
+    return buf
+
+
+def _upload_sparse_batch(batch, c: int, h: int, w: int, dev):
+    """The batch's CHW node tensors as one device node buffer + global segment offsets
+    (packed into pinned staging, one H2D each), or None when a stored node has value
+    +-0.0 (checked on the device: the dense batched path cannot represent it)."""
+    import torch
+
+    arrs = [np.asarray(t.nodes).view(np.int32).reshape(-1, 2) for t in batch]
+    counts = np.array([a.shape[0] for a in arrs], np.int64)
+    total = int(counts.sum())
+    hn = _pinned("nodes", total * 8)[: total * 8].view(torch.int32).view(-1, 2)
+    if total:
+        np.concatenate(arrs, out=hn.numpy())
+    hs = _pinned("seg", len(batch) * h * w * 8)[: len(batch) * h * w * 8].view(torch.int64).view(len(batch), h * w)
+    np.stack([np.asarray(t.segment_offsets, np.int64) for t in batch], out=hs.numpy())
+    nodes = torch.empty((max(total, 1), 2), dtype=torch.int32, device=dev)
+    if total:
+        nodes[:total].copy_(hn, non_blocking=True)
+    seg = hs.to(dev, non_blocking=True)
+    base = torch.from_numpy(np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)).to(dev)
+    seg += base.view(-1, 1)
+    # a stored zero (index >= 0, value bits +-0.0) cannot travel as a dense plane
+    if total and bool(((nodes[:total, 0] >= 0) & ((nodes[:total, 1] & 0x7FFFFFFF) == 0)).any()):
+        return None
+    return nodes[:total] if total else nodes[:0], seg.view(-1)
+
+
+def _step_bias(step: _Step, dev):
+    """The step's bias on the device (cached on the step)."""
+    import torch
+
+    b = getattr(step, "_dev_bias", None)
+    if b is None:
+        b = step._dev_bias = torch.from_numpy(np.ascontiguousarray(step.bias, np.float32)).to(dev)
+    return b
+
+
+def _step_bank(step: _Step, kind: str):
+    """A device re-layout of the step's filters for one sparse-input kernel ('fast',
+    'strip' or 'gather'), packed once and cached on the step."""
+    from . import device
+
+    banks = getattr(step, "_dev_banks", None)
+    if banks is None:
+        banks = step._dev_banks = {}
+    if kind not in banks:
+        pack = {"fast": device.si_pack_fast, "strip": device.si_pack3x3, "gather": device.kcrs_to_crsk}[kind]
+        banks[kind] = pack(_step_filters(step))
+    return banks[kind]
 
 
 def _step_filters(step: _Step):
@@ -456,12 +515,10 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
     c, h, w = prepared.net.input_dims
     dev = torch.device("cuda", torch.cuda.current_device())
     if variant == VARIANT_SPARSE_INPUT:
-        counts = [len(t.nodes) for t in batch]
-        base = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-        nodes = device.nodes_from_numpy(np.concatenate([np.asarray(t.nodes) for t in batch]))
-        seg = torch.from_numpy(np.concatenate([np.asarray(t.segment_offsets, np.int64) + b
-                                               for t, b in zip(batch, base)])).to(dev)
-        x = device.decode_order(nodes, seg, (n, c, h, w), "CHW")
+        up = _upload_sparse_batch(batch, c, h, w, dev)
+        if up is None:
+            return None
+        x = device.decode_order(up[0], up[1], (n, c, h, w), "CHW")
         sparse = True
     else:
         whc = torch.from_numpy(np.stack([np.asarray(t.data, np.float32) for t in batch])).to(dev)
@@ -478,7 +535,7 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
                 kcrs = _step_filters(step)
                 k, c_f, h_f, w_f = (int(v) for v in kcrs.shape)
             geom = ConvGeometry(dims, (c_f, h_f, w_f), step.stride, step.padding)
-            bias = torch.from_numpy(np.ascontiguousarray(step.bias, np.float32)).to(dev)
+            bias = _step_bias(step, dev)
             if sparse:
                 enc = device.encode_order(x, "CHW")
                 _, ci, hi, wi = (int(v) for v in x.shape)
@@ -490,13 +547,13 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
                     if step.fused_pool is not None and tuple(step.fused_pool) == (2, 2) and hi % 2 == 0 \
                             and wi % 2 == 0:
                         fp = "max" if step.fused_pool_mode == ly.POOL_MAX else "avg"
-                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack_fast(kcrs), k,
+                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "fast"), k,
                                                pool=fp)
                     fused = fp is not None
                 elif (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
-                    y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, device.si_pack3x3(kcrs), k)
+                    y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "strip"), k)
                 else:
-                    y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, device.kcrs_to_crsk(kcrs), k, h_f,
+                    y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "gather"), k, h_f,
                                        w_f, step.stride, step.padding)
                 if step.fused_pool is not None and not fused:
                     h_p, w_p = ly._pool_args(step.fused_pool, step.fused_pool_mode, geom.n_h, geom.n_w)
@@ -609,9 +666,10 @@ def forward(prepared: PreparedNet, batch: list, workers: int = 1,
     if prepared.engine is not None and not record_density:
         with _engine_lock:
             outputs = _forward_engine(prepared, batch)
-    elif _BATCHED and _batched_inputs_ok(prepared, batch):
-        outputs = _forward_batched(prepared, batch, densities)
     else:
+        outputs = _forward_batched(prepared, batch, densities) \
+            if _BATCHED and _batched_inputs_ok(prepared, batch) else None
+    if outputs is None:
         if not prepared.steps:
             raise NotImplementedError("per-layer execution needs a PreparedNet from prepare()")
         outputs = []

@@ -202,8 +202,13 @@ def test_batched_forward_equals_per_image(g, monkeypatch, exact):
                 live = np.flatnonzero(nodes["index"] >= 0)
                 nodes["value"][live[0]] = 0.0  # an explicit zero node
                 z = fs.SparseTensor3(t.order, t.dims, nodes, t.matrix_offsets, t.segment_offsets)
-                assert not nwmod._batched_inputs_ok(prepared, [z])
-                nw.forward(prepared, [z])  # per-image path
+                # the batched path declines it (device-side check) ...
+                assert nwmod._forward_batched(prepared, [z, inp[1]]) is None
+                # ... and forward() falls back to the per-image path, whose result it is
+                got = nw.forward(prepared, [z, inp[1]]).outputs
+                want = per_image(prepared, [z, inp[1]]).outputs
+                for a, b in zip(got, want):
+                    _same_output(a, b, key)
     finally:
         fs.set_exact(False)
 
