@@ -704,6 +704,23 @@ struct Group {
     int regs = 0;
 };
 
+// Filters per group from the bank's density: 48 (measured best at 90 % zeros on the
+// VGG16 stack), 64 for banks at <= 7 % density when that plan still runs >= 10 warps per
+// CTA -- at 95 % zeros a 48-filter channel block is ~21 FFMA2 against the same 12 patch
+// loads, and 64 filters measured L1/L3 -21 %, L5 -9 %, L10 -8 % (L7-L9 fall to 7 warps
+// and keep 48).  An explicit KT (flags, FSCNN_SFJIT_KT) wins.
+int pick_flags(const float *wt, int c, int k, int h, int w, int relu, int pool, int flags) {
+    if ((flags & 0xff) || getenv("FSCNN_SFJIT_KT")) return flags;
+    const int64_t n = (int64_t)k * c * 9;
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < n; ++i) nnz += wt[i] != 0.0f;
+    if (nnz * 100 > n * 7 || k <= 48) return flags;
+    Plan p;
+    char why[160];
+    if (make_plan(p, c, k, h, w, relu, pool, flags | 64, why, sizeof(why)) && p.WARPS >= 10) return flags | 64;
+    return flags;
+}
+
 }  // namespace
 }  // namespace fscnn
 
@@ -743,6 +760,7 @@ int fscnn_sfjit_create(const float *w_kc33, const float *bias, int k, int c, int
     FSCNN_REQUIRE(k > 0 && c > 0 && h > 0 && w > 0, "bad extents");
     auto j = std::make_unique<fscnn_sfjit>();
     char why[160];
+    flags = pick_flags(w_kc33, c, k, h, w, relu, pool, flags);
     if (!make_plan(j->plan, c, k, h, w, relu, pool, flags, why, sizeof(why))) {
         set_error("sfjit: %s", why);
         return FSCNN_ERR_UNSUPPORTED;
@@ -983,6 +1001,7 @@ int64_t fscnn_sfjit_ptx(const float *w_kc33, const float *bias, int k, int c, in
     if (!w_kc33 || k <= 0 || c <= 0) return -1;
     Plan p;
     char why[160];
+    flags = pick_flags(w_kc33, c, k, h, w, relu, pool, flags);
     if (!make_plan(p, c, k, h, w, relu, pool, flags, why, sizeof(why))) {
         set_error("sfjit: %s", why);
         return -1;

@@ -116,7 +116,12 @@ class VGGEngine:
             if jit and h % 2 == 0:
                 # compile jobs are submitted here and run on host threads while the next
                 # banks are encoded; the first forward joins them
-                step.jit = device.SfJit(dense, bias_t, h, h, relu=True, pool=pool)
+                # 48 filters per group: the whole stack's best with its batch parts running
+                # concurrently (the layer-alone density rule of sfjit.cu's pick_flags, 64 at
+                # <= 7 % density, measured 10 % slower per C5 step although each layer alone
+                # runs faster)
+                kt = 0 if os.environ.get("FSCNN_SFJIT_KT") else 48
+                step.jit = device.SfJit(dense, bias_t, h, h, relu=True, pool=pool, flags=kt)
             self.steps.append(step)
             c = k
             if pool:
@@ -174,7 +179,9 @@ class VGGEngine:
             return int(os.environ["FSCNN_PARTS"])
         if not (self._jit_all and n >= SFJIT_MIN_BATCH):
             return 2
-        return 8 if n >= 64 else 4
+        # more parts = later parts find the code earlier ones fetched (C3 @ 32: 4 parts;
+        # C5 @ 256: 8 -> 16 parts measured 12.4k -> 14.2k img/s)
+        return 16 if n >= 128 else 8 if n >= 64 else 4
 
     def _run(self, first: int, xin: torch.Tensor, parts: int) -> torch.Tensor:
         """_run_from through a CUDA graph captured once per (batch, entry layer, buffer):
