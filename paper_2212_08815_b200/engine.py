@@ -179,9 +179,9 @@ class VGGEngine:
             return int(os.environ["FSCNN_PARTS"])
         if not (self._jit_all and n >= SFJIT_MIN_BATCH):
             return 2
-        # more parts = later parts find the code earlier ones fetched (C3 @ 32: 4 parts;
-        # C5 @ 256: 8 -> 16 parts measured 12.4k -> 14.2k img/s)
-        return 16 if n >= 128 else 8 if n >= 64 else 4
+        # more parts = later parts find the code earlier ones fetched (C3 @ 32: 4 -> 8
+        # parts 8.73k -> 8.82k img/s; C5 @ 256: 8 -> 16 parts 12.4k -> 14.2k img/s)
+        return 16 if n >= 128 else 8 if n >= 32 else 4
 
     def _run(self, first: int, xin: torch.Tensor, parts: int) -> torch.Tensor:
         """_run_from through a CUDA graph captured once per (batch, entry layer, buffer):
