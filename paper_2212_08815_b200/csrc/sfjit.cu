@@ -533,7 +533,9 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
             // two moves it needs: it rematerialises the pair per use)
             for (int r = 0; r < 3; ++r) {
                 if (!odd_row[r] || p.odd_mode == 2) continue;
-                if (p.odd_mode == 0)
+                if (p.odd_mode == 3)  // debug: one aligned 8-byte load (wrong values) -- the cost of a shifted plane
+                    o("ld.shared.b64 od%d, [rb+%lld];", r, (long long)(off0 + (int64_t)r * p.P * 4 + 16));
+                else if (p.odd_mode == 0)
                     o("{ .reg .f32 x1, x2; ld.shared.f32 x1, [rb+%lld]; ld.shared.f32 x2, [rb+%lld]; mov.b64 od%d, "
                       "{x1, x2}; }",
                       (long long)(off0 + (int64_t)r * p.P * 4 + 4), (long long)(off0 + (int64_t)r * p.P * 4 + 8), r);
