@@ -456,10 +456,23 @@ def _upload_sparse_batch(batch, c: int, h: int, w: int, dev):
     seg = hs.to(dev, non_blocking=True)
     base = torch.from_numpy(np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)).to(dev)
     seg += base.view(-1, 1)
-    # a stored zero (index >= 0, value bits +-0.0) cannot travel as a dense plane
-    if total and bool(((nodes[:total, 0] >= 0) & ((nodes[:total, 1] & 0x7FFFFFFF) == 0)).any()):
+    # one device check, one sync: a stored zero (index >= 0, value bits +-0.0) cannot
+    # travel as a dense plane, and the structure must be what the decoder walks (each
+    # segment's channels ascending in [0, c), its sentinel right before the next
+    # segment's offset); otherwise the per-image path runs and its validate() reports
+    seg = seg.view(-1)
+    if not total:
         return None
-    return nodes[:total] if total else nodes[:0], seg.view(-1)
+    idx = nodes[:total, 0]
+    bad = ((idx >= 0) & ((nodes[:total, 1] & 0x7FFFFFFF) == 0)).any()
+    bad |= (idx >= c).any() | (idx < -1).any() | (idx[total - 1] != -1)
+    bad |= ((idx[1:] <= idx[:-1]) & (idx[1:] >= 0) & (idx[:-1] >= 0)).any()
+    bad |= (seg[0] != 0) | (seg[1:] <= seg[:-1]).any() | (seg[-1] >= total)
+    bad |= (idx[(seg[1:] - 1).clamp(0, total - 1)] != -1).any()
+    bad |= (idx == -1).sum() != seg.numel()
+    if bool(bad):
+        return None
+    return nodes[:total], seg
 
 
 def _step_bias(step: _Step, dev):

@@ -209,6 +209,19 @@ def test_batched_forward_equals_per_image(g, monkeypatch, exact):
                 want = per_image(prepared, [z, inp[1]]).outputs
                 for a, b in zip(got, want):
                     _same_output(a, b, key)
+                # malformed structure (two live nodes of a segment out of channel order):
+                # the batched path declines it on the device and the per-image path's
+                # validation reports it, as the reference's format check would
+                bad = t.nodes.copy()
+                seg0 = int(t.segment_offsets[0])
+                run = np.flatnonzero(bad["index"][seg0:] >= 0)
+                j = next(r for r in range(len(run) - 1) if run[r + 1] == run[r] + 1)
+                a0, a1 = seg0 + run[j], seg0 + run[j + 1]
+                bad["index"][a0], bad["index"][a1] = bad["index"][a1], bad["index"][a0]
+                zb = fs.SparseTensor3(t.order, t.dims, bad, t.matrix_offsets, t.segment_offsets)
+                assert nwmod._forward_batched(prepared, [zb]) is None
+                with pytest.raises(fs.FormatError):
+                    nw.forward(prepared, [zb])
     finally:
         fs.set_exact(False)
 
