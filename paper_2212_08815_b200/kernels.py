@@ -81,7 +81,13 @@ def _torch():
 
 
 def dense_to_device(t: DenseTensor3):
-    """Host DenseTensor3 (W,H,C memory) -> device NCHW [1, C, H, W] (GPU transpose)."""
+    """Host DenseTensor3 (W,H,C memory) -> device NCHW [1, C, H, W] (GPU transpose); a
+    DeviceDenseTensor3 is already that tensor."""
+    from .sparse_core import DeviceDenseTensor3
+
+    if isinstance(t, DeviceDenseTensor3):
+        t.validate()
+        return t.data
     torch = _torch()
     from . import device
 
@@ -90,9 +96,16 @@ def dense_to_device(t: DenseTensor3):
     return device.whc_to_nchw(flat, 1, c, h, w)
 
 
-def dense_from_device(y) -> DenseTensor3:
-    """Device [1, K, H, W] -> host DenseTensor3 (GPU transpose to W,H,C, then D2H)."""
+def dense_from_device(y, resident: bool = False) -> DenseTensor3:
+    """Device [1, K, H, W] -> host DenseTensor3 (GPU transpose to W,H,C, then D2H), or
+    (resident) a DeviceDenseTensor3 around it."""
     from . import device
+
+    if resident:
+        from .sparse_core import DeviceDenseTensor3
+
+        y = y.contiguous()
+        return DeviceDenseTensor3(tuple(int(v) for v in y.shape[1:]), y)
 
     _, k, h, w = (int(v) for v in y.shape)
     whc = device.nchw_to_whc(y)
@@ -103,6 +116,11 @@ def sparse_to_device(t: SparseTensor3):
     """Host SparseTensor3 -> (device nodes, device segment offsets).  The structure is
     validated first (sorted in-range indices, sentinel-terminated segments): the kernels
     trust it, and a malformed fiber would index shared memory out of bounds."""
+    from .sparse_core import DeviceSparseTensor3
+
+    if isinstance(t, DeviceSparseTensor3):
+        t.validate()
+        return t.nodes, t.segment_offsets
     torch = _torch()
     from . import device
 

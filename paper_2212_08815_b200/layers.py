@@ -26,13 +26,24 @@ from .sparse_core import (
     AxisOrder2,
     AxisOrder3,
     DenseTensor3,
+    DeviceDenseTensor3,
+    DeviceSparseTensor3,
     SparseMatrix,
     SparseTensor3,
     SparseTensor4,
+    _sparse_result,
 )
 
 POOL_MAX = "max"
 POOL_AVG = "avg"
+
+_DENSE = (DenseTensor3, DeviceDenseTensor3)
+_SPARSE = (SparseTensor3, DeviceSparseTensor3)
+
+
+def _resident(t) -> bool:
+    """A device twin in means a device twin out (the chain stays on the GPU)."""
+    return isinstance(t, (DeviceDenseTensor3, DeviceSparseTensor3))
 
 _EXACT = os.environ.get("FSCNN_EXACT", "0") == "1"
 
@@ -194,7 +205,7 @@ def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: 
         # the jump-table kernel.  Compiled on first use, cached with the bank.
         jit = _layer_jit(filters, bias, h, w)
         y = device.from_halo(jit(device.to_halo(x)), w).contiguous()
-        return kernels.dense_from_device(y)
+        return kernels.dense_from_device(y, _resident(t_in))
     if packed is not None and stride == 1 and padding == 1 and not _EXACT:
         # the fast kernel, with its small-grid plan (fewer filters per warp, more CTAs)
         # when the default grid would leave SMs idle -- one image of config 1: 11.9 us
@@ -206,7 +217,7 @@ def _sf_layer(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: 
     else:
         _, h_f, w_f = filters.dims[1:]
         y = device.sf_conv_exact(x, nodes, seg, k, h_f, w_f, stride, padding, b)
-    return kernels.dense_from_device(y)
+    return kernels.dense_from_device(y, _resident(t_in))
 
 
 def conv_forward_strategy_I(t_in: DenseTensor3, filters: SparseTensor4, stride: int, padding: int,
@@ -281,11 +292,8 @@ def conv_forward_sparse_input(t_in: SparseTensor3, filters: list[DenseTensor3], 
     bias = np.asarray(bias, dtype=np.float32)
     if np.any(bias != 0):
         y = y + torch.from_numpy(bias).cuda().view(1, -1, 1, 1)
-        return kernels.dense_from_device(y)
-    enc = device.encode_order(y, "CHW")
-    k, n_h, n_w = (int(v) for v in y.shape[1:])
-    return SparseTensor3(AxisOrder3.CHW, (k, n_h, n_w), device.nodes_to_numpy(enc.nodes, enc.n_nodes),
-                         enc.matrix_off.cpu().numpy(), enc.seg_off.cpu().numpy())
+        return kernels.dense_from_device(y, _resident(t_in))
+    return _sparse_result(device.encode_order(y, "CHW"), AxisOrder3.CHW, y.shape[1:], _resident(t_in))
 
 
 def merged_conv_pool(t_in: SparseTensor3, t_f: DenseTensor3, stride: int, pool, mode: str,
@@ -319,7 +327,7 @@ def pool_standalone(t: DenseTensor3, pool, mode: str) -> DenseTensor3:
     if mode not in (POOL_MAX, POOL_AVG):
         raise ValueError(f"unknown pool mode {mode!r}")
     y = device.pool2d(kernels.dense_to_device(t), h_p, w_p, mode == POOL_MAX)
-    return kernels.dense_from_device(y)
+    return kernels.dense_from_device(y, _resident(t))
 
 
 def pool_sparse(t: SparseTensor3, pool, mode: str) -> SparseTensor3:
@@ -337,7 +345,7 @@ def pool_sparse(t: SparseTensor3, pool, mode: str) -> SparseTensor3:
     if mode not in (POOL_MAX, POOL_AVG):
         raise ValueError(f"unknown pool mode {mode!r}")
     y = device.pool2d(to_device_dense(t), h_p, w_p, mode == POOL_MAX)
-    return from_device_dense(y, t.order)
+    return from_device_dense(y, t.order, _resident(t))
 
 
 def apply_activation(t, kind: str, slope: float = 0.0):
@@ -355,15 +363,19 @@ def apply_activation(t, kind: str, slope: float = 0.0):
         raise ValueError("leaky slope must be non-negative")
     from . import device
 
+    if isinstance(t, DeviceDenseTensor3):
+        t.validate()
+        y = device.activation(t.data, device.ACT_RELU if kind == "relu" else device.ACT_LEAKY, slope)
+        return DeviceDenseTensor3(tuple(t.dims), y)
     if isinstance(t, DenseTensor3):
         flat = kernels._torch().from_numpy(np.ascontiguousarray(t.data)).cuda()
         y = device.activation(flat, device.ACT_RELU if kind == "relu" else device.ACT_LEAKY, slope)
         return DenseTensor3(tuple(t.dims), y.cpu().numpy())
-    if isinstance(t, SparseTensor3):
+    if isinstance(t, _SPARSE):
         from .sparse_core import from_device_dense, to_device_dense
 
         act = device.ACT_RELU_NODES if kind == "relu" else device.ACT_LEAKY
-        return from_device_dense(device.activation(to_device_dense(t), act, slope), t.order)
+        return from_device_dense(device.activation(to_device_dense(t), act, slope), t.order, _resident(t))
     raise TypeError(f"apply_activation does not support {type(t).__name__}")
 
 
@@ -396,17 +408,17 @@ def apply_batchnorm(t, params: BatchNormParams):
     from . import device
 
     params.validate(t.dims[0])
-    if isinstance(t, SparseTensor3):
+    if isinstance(t, _SPARSE):
         from .sparse_core import from_device_dense, to_device_dense
 
         y = device.batchnorm(to_device_dense(t), params.scale, params.shift, params.mean, params.var,
                              params.epsilon)
-        return from_device_dense(y, t.order)
-    if not isinstance(t, DenseTensor3):
+        return from_device_dense(y, t.order, _resident(t))
+    if not isinstance(t, _DENSE):
         raise TypeError(f"apply_batchnorm does not support {type(t).__name__}")
     y = device.batchnorm(kernels.dense_to_device(t), params.scale, params.shift, params.mean, params.var,
                          params.epsilon)
-    return kernels.dense_from_device(y)
+    return kernels.dense_from_device(y, _resident(t))
 
 
 def pad_tensor(t, p: int):
@@ -418,13 +430,13 @@ def pad_tensor(t, p: int):
         return t
     from . import device
 
-    if isinstance(t, DenseTensor3):
-        return kernels.dense_from_device(device.pad2d(kernels.dense_to_device(t), p))
-    if isinstance(t, SparseTensor3):
+    if isinstance(t, _DENSE):
+        return kernels.dense_from_device(device.pad2d(kernels.dense_to_device(t), p), _resident(t))
+    if isinstance(t, _SPARSE):
         from .sparse_core import from_device_dense, to_device_dense
 
         if t.order is not AxisOrder3.CHW:
-            return from_device_dense(device.pad2d(to_device_dense(t), p), t.order)
+            return from_device_dense(device.pad2d(to_device_dense(t), p), t.order, _resident(t))
         torch = kernels._torch()
         c, h, w = t.dims
         nh, nw = h + 2 * p, w + 2 * p
@@ -433,9 +445,10 @@ def pad_tensor(t, p: int):
         hi = torch.arange(nh, device="cuda").view(1, nh) - p
         inside = (wi >= 0) & (wi < w) & (hi >= 0) & (hi < h)
         seg_map = torch.where(inside, wi * h + hi, torch.full_like(wi * hi, -1)).view(-1)
-        nodes, n_nodes = device.nodes_from_numpy(t.nodes), len(t.nodes)
-        seg = torch.from_numpy(np.asarray(t.segment_offsets, np.int64)).cuda()
-        out, count, off = device.remap_segments(nodes, seg, n_nodes, seg_map)
+        nodes, seg = kernels.sparse_to_device(t)
+        out, count, off = device.remap_segments(nodes, seg, int(nodes.shape[0]), seg_map)
+        if _resident(t):
+            return DeviceSparseTensor3(t.order, (c, nh, nw), out[:count], off[::nh].clone(), off)
         off_h = off.cpu().numpy()
         return SparseTensor3(t.order, (c, nh, nw), device.nodes_to_numpy(out, count), off_h[::nh].copy(), off_h)
     raise TypeError(f"pad_tensor does not support {type(t).__name__}")
@@ -451,4 +464,4 @@ def conv_forward_dense(t_in: DenseTensor3, filters: list[DenseTensor3], stride: 
     kcrs = kernels.filters_to_device_kcrs(filters)
     b = kernels._torch().from_numpy(np.ascontiguousarray(bias, dtype=np.float32)).cuda()
     y = device.dense_conv_exact(kernels.dense_to_device(t_in), kcrs, geom.stride, geom.padding, b)
-    return kernels.dense_from_device(y)
+    return kernels.dense_from_device(y, _resident(t_in))
