@@ -134,6 +134,11 @@ class ShardedVGG:
         cdev = comm_device(self.device, group)
         if self.rank == 0:
             eng0 = VGGEngine(layers, batch=1, hw=hw, plan=plan, in_c=in_c)
+            if self.world > 1:
+                # rank 0 compiles the specialised kernels alone while the other ranks wait
+                # in the broadcast; they then find every cubin in the shared disk cache
+                # (same PTX on every rank) instead of all ranks compiling the same code
+                eng0.wait_compiled()
             banks = [(s.nodes[: s.n_nodes], s.seg_off, s.tensor_off, s.matrix_off, s.bias) for s in eng0.steps]
             banks = [tuple(t.to(cdev) for t in b) for b in banks]
         else:
