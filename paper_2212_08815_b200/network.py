@@ -424,6 +424,7 @@ def _batched_inputs_ok(prepared: PreparedNet, batch) -> bool:
 
 
 _pinned_in: dict = {}  # grow-only pinned staging for the sparse-input batch upload
+_pinned_lock = threading.Lock()  # forward() may run on several host threads
 
 
 def _pinned(key: str, nbytes: int):
@@ -440,6 +441,13 @@ def _upload_sparse_batch(batch, c: int, h: int, w: int, dev):
     """The batch's CHW node tensors as one device node buffer + global segment offsets
     (packed into pinned staging, one H2D each), or None when a stored node has value
     +-0.0 (checked on the device: the dense batched path cannot represent it)."""
+    import torch
+
+    with _pinned_lock:  # the staging is reused: held until the copies have completed
+        return _upload_sparse_batch_locked(batch, c, h, w, dev)
+
+
+def _upload_sparse_batch_locked(batch, c: int, h: int, w: int, dev):
     import torch
 
     arrs = [np.asarray(t.nodes).view(np.int32).reshape(-1, 2) for t in batch]
@@ -462,6 +470,7 @@ def _upload_sparse_batch(batch, c: int, h: int, w: int, dev):
     # segment's offset); otherwise the per-image path runs and its validate() reports
     seg = seg.view(-1)
     if not total:
+        torch.cuda.current_stream().synchronize()  # the pinned staging is free again
         return None
     idx = nodes[:total, 0]
     bad = ((idx >= 0) & ((nodes[:total, 1] & 0x7FFFFFFF) == 0)).any()
