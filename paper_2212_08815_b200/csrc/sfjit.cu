@@ -917,7 +917,8 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
         note_launch(1);
         return FSCNN_OK;
     }
-    const int n_side = (int)std::min<size_t>(j->groups.size(), 16);
+    static const int max_side = getenv("FSCNN_SFJIT_STREAMS") ? atoi(getenv("FSCNN_SFJIT_STREAMS")) : 16;
+    const int n_side = (int)std::min<size_t>(j->groups.size(), (size_t)std::max(1, max_side));
     fscnn_sfjit::Side *sd = nullptr;
     for (auto &e : j->sides)
         if (e.first == cs) sd = &e.second;
