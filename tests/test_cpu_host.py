@@ -324,3 +324,43 @@ def test_sfjit_generator_emits_valid_ptx_and_compiles():
     w = np.ones((8, 4, 3, 3), np.float32)
     assert lib.fscnn_sfjit_ptx(w.ctypes.data, None, 8, 4, 15, 15, 1, 0, 0, 0, None, 0) == -1
     assert b"even" in lib.fscnn_last_error()
+
+
+def test_device_twin_host_logic():
+    """Device twins: host tensors pass through to_host, unsupported
+    types are refused, and DeviceSparseTensor3.validate applies the host validate()'s
+    rules (exercised here on CPU torch tensors holding a reference-encoded tensor)."""
+    import torch
+
+    t = fs.DenseTensor3.from_array(np.zeros((2, 3, 4), np.float32))
+    assert fs.to_host(t) is t
+    with pytest.raises(TypeError):
+        fs.to_device(np.zeros(3))
+    # a 2-channel 2x2 CHW tensor: segments (w*H + h) each a channel fiber + sentinel
+    nodes = np.array([(0, 1.0), (1, 2.0), (-1, 0.0), (-1, 0.0), (1, 3.0), (-1, 0.0), (0, 4.0), (-1, 0.0)],
+                     dtype=fs.NODE_DTYPE)
+    seg = np.array([0, 3, 4, 6], np.int64)
+    host = fs.SparseTensor3(fs.AxisOrder3.CHW, (2, 2, 2), nodes, seg[::2].copy(), seg)
+    host.validate()
+
+    def twin(nd, sg, mat=None):
+        words = torch.from_numpy(np.ascontiguousarray(nd).view(np.int32).reshape(-1, 2).copy())
+        sg_t = torch.from_numpy(np.asarray(sg, np.int64))
+        return fs.DeviceSparseTensor3(fs.AxisOrder3.CHW, (2, 2, 2), words,
+                                      sg_t[::2].clone() if mat is None else torch.tensor(mat), sg_t)
+
+    d = twin(nodes, seg)
+    d.validate()
+    assert d.n_segments == 4 and d.nnz == 4
+    bad = nodes.copy()
+    bad["index"][0], bad["index"][1] = 1, 0  # channels out of order
+    with pytest.raises(fs.FormatError, match="increase"):
+        twin(bad, seg).validate()
+    with pytest.raises(fs.FormatError, match="strictly increase"):
+        twin(nodes, [0, 3, 3, 6]).validate()
+    bad = nodes.copy()
+    bad["index"][4] = 2  # out of [0, C)
+    with pytest.raises(fs.FormatError, match="out of"):
+        twin(bad, seg).validate()
+    with pytest.raises(fs.FormatError, match="matrix"):
+        twin(nodes, seg, mat=[0, 3]).validate()
