@@ -256,13 +256,13 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     }
     p.WARPS = (p.TI + 31) / 32;
     p.T = 32 * p.WARPS;
-    // row pitch: >= w + 2 (memory columns 0..w+1 of the halo layout: every real lane's
-    // patch), 16-byte multiple (TMA box width); lanes of a padded tile row read past it
-    // into the next row (or <= 8 bytes past the box) and store nothing.  Sizing by the
-    // real width, not the padded one, shrinks the 14x14 layers' boxes 3x (pitch 48 -> 16:
-    // 3x the channels per chunk).  With BW < 16 a half-warp covers both rows of a row
-    // pair, whose 8-byte patch loads stay on distinct banks when pitch/2 == 8 (mod 16)
-    p.P = (int)align_up((getenv("FSCNN_SFJIT_PADP") ? 2 * p.TPR : w) + 2, 4);
+    // row pitch: >= 2 TPR + 2 (the padded tile row's patches; w + 2 would cover every real
+    // lane -- padded lanes then read into the next row and store nothing -- and shrinks
+    // the 14x14 boxes 3x, but measured -1..-2 % at 90 % zeros and +2..4 % at 50 % on
+    // L10/L11: FSCNN_SFJIT_REALP=1), 16-byte multiple (TMA box width).  With BW < 16 a
+    // half-warp covers both rows of a row pair, whose 8-byte patch loads stay on distinct
+    // banks when pitch/2 == 8 (mod 16)
+    p.P = (int)align_up((getenv("FSCNN_SFJIT_REALP") ? w : 2 * p.TPR) + 2, 4);
     if (p.BW < 16)
         while (p.P % 32 != 16) p.P += 4;
     if (p.P > 256) {
