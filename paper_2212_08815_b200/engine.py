@@ -307,10 +307,17 @@ class VGGEngine:
         cur = torch.cuda.current_stream()
         cp = self._copy_stream
         cp.wait_stream(cur)  # the previous call's readers of _d_in are done
+        # copy parts x head convs measured (bench e2e, batch 32): 4 x 2 8031 img/s, 4 x 1
+        # 7855, 8 x 2 7877, 2 x 2 7941, 16 x 2 7644, 1 x 1 7701 (profiles/r02_e2e_parts.txt)
         parts = 4 if n >= 8 else (2 if n >= 2 else 1)
+        if os.environ.get("FSCNN_E2E_PARTS"):
+            parts = max(1, min(n, int(os.environ["FSCNN_E2E_PARTS"])))
         halves = [(n * j // parts, n * (j + 1) // parts) for j in range(parts)]
-        events = []
-        first = self.steps[0]
+        # the first two convs (the 224x224 block, ~12 % of the stack) run per copy part as
+        # soon as it lands, hiding more of the H2D behind them (FSCNN_E2E_HEAD=1 keeps only
+        # the first conv there)
+        head = 1 if os.environ.get("FSCNN_E2E_HEAD") == "1" or len(self.steps) < 3 else 2
+        w = self.hw
         for lo, hi in halves:
             if fill is not None:
                 fill(lo, hi)
@@ -321,9 +328,13 @@ class VGGEngine:
             cur.wait_event(ev)
             device.whc_to_halo(self._d_in[lo * elems:hi * elems], hi - lo, self.in_c, self.hw, self.hw,
                                self._in[lo:hi])
-            first.conv(self._in[lo:hi], bufs[0][lo:hi], self.hw, n)
-        tail = self._run(1, bufs[0], self.parts_for(n)) if graphed_tail else \
-            self._run_from(1, bufs[0], self.parts_for(n))
+            x, w = self._in[lo:hi], self.hw
+            for i in range(head):
+                self.steps[i].conv(x, bufs[i][lo:hi], w, n)
+                x = bufs[i][lo:hi]
+                w = w // 2 if self.steps[i].pool else w
+        tail = self._run(head, bufs[head - 1], self.parts_for(n)) if graphed_tail else \
+            self._run_from(head, bufs[head - 1], self.parts_for(n))
         return device.halo_to_whc(tail, self.out_hw)
 
     def run_exact(self, x: torch.Tensor) -> torch.Tensor:
