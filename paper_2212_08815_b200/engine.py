@@ -120,7 +120,11 @@ class VGGEngine:
                 # concurrently (the layer-alone density rule of sfjit.cu's pick_flags, 64 at
                 # <= 7 % density, measured 10 % slower per C5 step although each layer alone
                 # runs faster)
-                kt = 0 if os.environ.get("FSCNN_SFJIT_KT") else 48
+                # ... except the shallow layers (C <= 64), run outside the batch parts (or per
+                # H2D part): 64-filter groups there (alone L1 -14 %, L2 -10 %;
+                # profiles/r02_sfjit_kt90.txt)
+                kt = 0 if os.environ.get("FSCNN_SFJIT_KT") else \
+                    (int(os.environ.get("FSCNN_SFJIT_SHALLOW_KT", "64")) if c <= 64 else 48)
                 step.jit = device.SfJit(dense, bias_t, h, h, relu=True, pool=pool, flags=kt)
             self.steps.append(step)
             c = k
@@ -227,6 +231,20 @@ class VGGEngine:
         for st in self.steps[:first]:
             w0 = w0 // 2 if st.pool else w0
         cur_stream = torch.cuda.current_stream()
+        serial = int(os.environ.get("FSCNN_SERIAL_HEAD", "2"))
+        if serial > first:
+            # the first two layers (224x224, 64 channels: small code, big grids) as
+            # full-batch launches on the current stream, with 64-filter groups (see
+            # __init__); the batch parts start at layer 2 (C3: value +0.7 %, e2e +2 %;
+            # profiles/r02_serial_head.txt)
+            cur, w = xin, w0
+            for st, out in zip(self.steps[first:serial], bufs[first:serial]):
+                st.conv(cur, out, w, n)
+                cur = out
+                w = w // 2 if st.pool else w
+            xin, w0, first = cur, w, serial
+            if first >= len(self.steps):
+                return bufs[-1]
         if parts > 1 and (getattr(self, "_split_streams", None) is None or len(self._split_streams) != parts):
             self._split_streams = [torch.cuda.Stream(device=xin.device) for _ in range(parts)]
         streams = self._split_streams if parts > 1 else [cur_stream]
