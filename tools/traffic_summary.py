@@ -1,6 +1,6 @@
 """Summarise the ncu launch list of tools/prof_forward.py (one eager VGG16 forward, one
 batch part, cold caches) into profiles/: sfjit launches grouped per layer (the engine
-launches a layer's ceil(K / 48) groups in order), kernel time and DRAM bytes per layer.
+launches a layer's ceil(K / KT) groups in order; KT = 64 on the C <= 64 layers, else 48), kernel time and DRAM bytes per layer.
 bench.py reads dram_bytes_per_layer from the result as the roofline's `traffic`.
 
 usage: python tools/traffic_summary.py launches.csv OUT.json
@@ -10,6 +10,9 @@ import json
 import sys
 
 KS = [64, 64, 128, 128, 256, 256, 256, 512, 512, 512, 512, 512, 512]
+CS = [3] + KS[:-1]
+# filters per group as the engine picks them: 64 on the shallow (C <= 64) layers, else 48
+KT = [64 if c <= 64 else 48 for c in CS]
 
 
 def main():
@@ -28,7 +31,7 @@ def main():
     dur = lambda L: L["gpu__time_duration.sum"] * 1e-6  # ns -> ms
     per_layer, pos = [], 0
     for li, k in enumerate(KS):
-        g = (k + 47) // 48
+        g = (k + KT[li] - 1) // KT[li]
         grp = jit[pos:pos + g]
         pos += g
         per_layer.append({"layer": li, "groups": g, "kernel_ns_sum": sum(L["gpu__time_duration.sum"] for L in grp),
