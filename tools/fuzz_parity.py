@@ -1,7 +1,8 @@
 """Seeded random-shape fuzz of the fast kernels against the bit-exact ones (which the
 tests pin to the reference): the sparse-filter kernel (every filters-per-warp / CTA
-plan, with and without the fused ReLU + pool) against the reference-order kernel, and
-the channel-major sparse-input kernel against the strip kernel.  Reports the worst
+plan, with and without the fused ReLU + pool) against the reference-order kernel, the
+specialised per-layer kernels (sfjit: per-group and fused modes) bit for bit against the
+jump-table kernel, and the channel-major sparse-input kernel against the strip kernel.  Reports the worst
 normwise error (north-star bar 1e-4) and any plan disagreement (must be bit-identical).
 
 usage: python tools/fuzz_parity.py [--cases 200] [--seed 1]
@@ -27,10 +28,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--sfjit-every", type=int, default=1, help="check the specialised kernels every Nth case (0: off)")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     worst_sf = worst_si = 0.0
     plan_mismatch = 0
+    sfjit_cases = sfjit_mismatch = 0
     for i in range(args.cases):
         n = int(rng.integers(1, 5))
         c = int(rng.choice([1, 3, 5, 16, 17, 33, 64, 100]))
@@ -58,6 +61,22 @@ def main():
                 yp = device.sf_conv3x3(xh, bank, bd, relu=True, pool=True, w=w, cta_warps=warps)
                 outs.append(device.from_halo(yp, w // 2).clone())
             outs.append(got.clone())
+        # the specialised kernels (per-group launches at 48 / 16 filters per group, and the
+        # fused one-kernel mode the layer API uses) on even extents: bit-identical to the
+        # jump-table kernel (same per-output order), pooled and not
+        if h % 2 == 0 and w % 2 == 0 and (args.sfjit_every and i % args.sfjit_every == 0):
+            base = outs[0] if not pool else outs[1]
+            for flags in (0, 16, 4 | (8 << 8) | (1 << 16)):
+                jit = device.SfJit(wd, bd, h, w, relu=True, pool=False, flags=flags).wait()
+                yj = device.from_halo(jit(xh), w)
+                sfjit_cases += 1
+                if not torch.equal(yj.contiguous().view(torch.int32), base.contiguous().view(torch.int32)):
+                    sfjit_mismatch += 1
+                if pool:
+                    jp = device.SfJit(wd, bd, h, w, relu=True, pool=True, flags=flags).wait()
+                    yp = device.from_halo(jp(xh), w // 2)
+                    if not torch.equal(yp.contiguous().view(torch.int32), outs[0].contiguous().view(torch.int32)):
+                        sfjit_mismatch += 1
         # all plans bit-identical
         per_plan = len(outs) // 5
         for j in range(1, 5):
@@ -75,8 +94,9 @@ def main():
         worst_si = max(worst_si, nerr(b, a))
     torch.cuda.synchronize()
     print(f"{args.cases} cases: worst normwise SF fast vs exact {worst_sf:.2e}, SI channel-major vs strip "
-          f"{worst_si:.2e}, plan mismatches {plan_mismatch}")
-    assert worst_sf <= 1e-4 and worst_si <= 1e-4 and plan_mismatch == 0
+          f"{worst_si:.2e}, plan mismatches {plan_mismatch}, specialised-kernel launches {sfjit_cases} "
+          f"with {sfjit_mismatch} mismatches vs the jump-table kernel")
+    assert worst_sf <= 1e-4 and worst_si <= 1e-4 and plan_mismatch == 0 and sfjit_mismatch == 0
 
 
 if __name__ == "__main__":
