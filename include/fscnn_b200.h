@@ -204,7 +204,11 @@ int fscnn_kcrs_to_crsk(const float *w_kcrs, int k, int c, int r, int s, float *w
  * strip of 8 outputs of one row and walks the strip's input columns left to right (the
  * reference's kw-outer order per output), applying each node to up to three outputs with
  * one 16-byte weight load.  wq: [c][kh][K] float4 {w(kw=0), w(kw=1), w(kw=2), 0} built
- * by fscnn_si_pack3x3 from a dense [K][C][3][3] bank (c*3*K float4 = 48*c*K bytes). */
+ * by fscnn_si_pack3x3 from a dense [K][C][3][3] bank (c*3*K float4 = 48*c*K bytes).
+ * The input must satisfy the format's invariant that segments are stored back to back
+ * (seg_off[s + 1] == seg_off[s] + count(s) + 1, sentinel last): one-image calls read a
+ * fiber's nodes up to seg_off[s + 1] - 1 in coalesced blocks (the Python layer validates
+ * this before calling). */
 int fscnn_si_pack3x3(const float *w_kc33, int k, int c, float *wq, void *stream);
 int fscnn_si_conv3x3(const fscnn_node *in_nodes, const int64_t *in_seg_off, int n, int c, int h,
                      int w, const float *wq, int k, const float *bias, float *y, void *stream);

@@ -33,6 +33,7 @@ from . import layers as ly
 from .sparse_core import (
     AxisOrder3,
     DenseTensor3,
+    NODE_DTYPE,
     FormatError,
     SparseTensor3,
     SparseTensor4,
@@ -463,6 +464,9 @@ def _pack_pool():
 def _upload_sparse_batch_locked(batch, c: int, h: int, w: int, dev):
     import torch
 
+    # shapes the dense batched path cannot take (the per-image path validates and reports)
+    if any(np.asarray(t.nodes).dtype != NODE_DTYPE or len(t.segment_offsets) != h * w for t in batch):
+        return None
     arrs = [np.asarray(t.nodes).view(np.int32).reshape(-1, 2) for t in batch]
     counts = np.array([a.shape[0] for a in arrs], np.int64)
     total = int(counts.sum())
