@@ -238,6 +238,14 @@ int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off,
 int fscnn_si_conv3x3_fast_pool(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,
                                int c, int h, int w, const float *wf, int k, const float *bias, int pool,
                                float *y, void *stream);
+/* The same conv (pool as above) straight from a dense activation x [n][c][h][w] (fp32,
+ * contiguous) instead of its CHW node encoding -- the result is bit-identical to
+ * encoding x (fscnn_encode_*: values +-0.0 not stored, NaN stored) and calling
+ * fscnn_si_conv3x3_fast_pool: the tile streams hold the same entries.  K >= 64.  Lets a
+ * stack of sparse-input layers skip the re-encode (count, scan, host sync, write)
+ * between layers. */
+int fscnn_si_conv3x3_fast_dense(const float *x, int n, int c, int h, int w, const float *wf, int k,
+                                const float *bias, int pool, float *y, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Dense layers between convolutions.

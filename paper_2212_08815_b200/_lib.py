@@ -52,6 +52,7 @@ _SIGNATURES = {
     "fscnn_si_pack_fast": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fscnn_si_conv3x3_fast": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp]),
     "fscnn_si_conv3x3_fast_pool": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
+    "fscnn_si_conv3x3_fast_dense": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
     "fscnn_dense_conv_exact": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fscnn_relu": (_i32, [_vp, _i64, _vp, _vp]),
     "fscnn_activation": (_i32, [_vp, _i64, _i32, ctypes.c_float, _vp, _vp]),

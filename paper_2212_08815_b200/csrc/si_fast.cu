@@ -410,6 +410,80 @@ __global__ void __launch_bounds__(SI_LW * 32) si_tile_lists_kernel(
     if (lane == 0) slots[link] = make_int2(kNP, -1);
 }
 
+// Pass 1 from a dense NCHW activation instead of nodes (the batched network forward: no
+// encode between layers).  The same stream, entry for entry: per live channel ascending,
+// the region positions whose value is stored by the reference encoder (value != +-0.0;
+// NaN kept -- sparsify_tensor3, sparse_core.py:334-353) in ascending position order, the
+// same links.  Lanes own region positions (a row of the window is contiguous); a count
+// pass sizes the tile's stream, a second pass writes it channel by channel (the dense
+// input gives each channel's entries and their ranks with one ballot, no shared memory).
+template <int TY, int TX>
+__global__ void __launch_bounds__(SI_LW * 32) si_tile_lists_dense_kernel(
+    const float *__restrict__ x, int c_n, int h, int w, int tiles_x, int tpi,
+    unsigned long long *__restrict__ slot_ctr, int64_t cap_slots, int64_t *__restrict__ tile_start,
+    int2 *__restrict__ slots) {
+    constexpr int kNP = SiTile<TY, TX>::NP, kRX = SiTile<TY, TX>::RX;
+    constexpr int kR = (kNP + 31) / 32;  // lane rounds over the region positions
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x * SI_LW + warp, img = blockIdx.y;
+    if (tile >= tpi) return;
+    const int ty0 = (tile / tiles_x) * TY, tx0 = (tile % tiles_x) * TX;
+    int64_t off[kR];  // this lane's position in a channel plane, or -1 outside the image
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        const int p = r * 32 + lane;
+        const int yy = ty0 - 1 + p / kRX, xx = tx0 - 1 + p % kRX;
+        off[r] = (p < kNP && yy >= 0 && yy < h && xx >= 0 && xx < w) ? (int64_t)yy * w + xx : -1;
+    }
+    const float *xi = x + (int64_t)img * c_n * h * w;
+    const int64_t plane = (int64_t)h * w;
+    auto stored = [&](int ch, int r) -> bool {
+        if (off[r] < 0) return false;
+        return (__float_as_uint(__ldg(xi + ch * plane + off[r])) & 0x7fffffffu) != 0u;
+    };
+    int64_t nnz = 0, live = 0;
+    for (int ch = 0; ch < c_n; ++ch) {
+        int k = 0;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) k += __popc(__ballot_sync(0xffffffffu, stored(ch, r)));
+        nnz += k;
+        live += k > 0;
+    }
+    int64_t base = 0;
+    if (lane == 0) {
+        const int64_t need = nnz + live + 1;
+        base = (int64_t)atomicAdd(slot_ctr, (unsigned long long)need);
+        if (base + need > cap_slots) base = -1;  // cannot happen: cap_slots bounds the sum
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    tile_start[(int64_t)img * tpi + tile] = base;
+    if (base < 0) return;
+    int64_t link = base, out = base + 1;
+    for (int ch = 0; ch < c_n; ++ch) {
+        unsigned m[kR];
+        float v[kR];
+        int k = 0;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            v[r] = off[r] >= 0 ? __ldg(xi + ch * plane + off[r]) : 0.0f;
+            m[r] = __ballot_sync(0xffffffffu, off[r] >= 0 && (__float_as_uint(v[r]) & 0x7fffffffu) != 0u);
+            k += __popc(m[r]);
+        }
+        if (!k) continue;
+        if (lane == 0) slots[link] = make_int2(kNP, ch);
+        int before = 0;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            if ((m[r] >> lane) & 1u)
+                slots[out + before + __popc(m[r] & ((1u << lane) - 1u))] = make_int2(r * 32 + lane, __float_as_int(v[r]));
+            before += __popc(m[r]);
+        }
+        link = out + k;
+        out += k + 1;
+    }
+    if (lane == 0) slots[link] = make_int2(kNP, -1);
+}
+
 // Epilogue of the two-pass kernel: + bias (and Alg. 7's fused 2x2 pool, layers.py:345-390,
 // in pool2d's order -- (ph, pw) row-major, max from -inf with '>', avg as a left-to-right
 // sum (first NaN wins) / 4 -- before the bias), a zero sum stored as +0.0 (no node in
@@ -615,8 +689,10 @@ inline SiWs si_ws(int n, int c, int h, int w, int64_t n_nodes) {
 
 template <int TY, int TX, int PAIRS, int NW, int MINB>
 int launch_tl(const int2 *nodes, const int64_t *seg_off, int64_t n_nodes, int n, int c, int h, int w,
-              const float *wf, int k, int kp, const float *bias, float *y, cudaStream_t st, int pool) {
-    const SiWs s = si_ws<TY, TX>(n, c, h, w, n_nodes);
+              const float *wf, int k, int kp, const float *bias, float *y, cudaStream_t st, int pool,
+              const float *x_dense = nullptr) {
+    // dense input: the node-count bound is the element count
+    const SiWs s = si_ws<TY, TX>(n, c, h, w, x_dense ? (int64_t)n * c * h * w : n_nodes);
     static bool pool_set = false;
     if (!pool_set) {
         // keep freed workspace in the stream-ordered pool (no OS round trip per call)
@@ -639,9 +715,16 @@ int launch_tl(const int2 *nodes, const int64_t *seg_off, int64_t n_nodes, int n,
     auto *ctr = reinterpret_cast<unsigned long long *>(ws);
     auto *ts = reinterpret_cast<int64_t *>(ws + s.off_ts);
     auto *slots = reinterpret_cast<int2 *>(ws + s.off_slots);
-    si_tile_lists_kernel<TY, TX><<<dim3((unsigned)ceil_div(tpi, SI_LW), (unsigned)n), SI_LW * 32, 0, st>>>(
-        nodes, seg_off, n_nodes, n, c, h, w, tiles_x, tpi, ctr, s.cap_slots, ts, slots);
-    int rc = check_launch("si_tile_lists_kernel");
+    int rc;
+    if (x_dense) {
+        si_tile_lists_dense_kernel<TY, TX><<<dim3((unsigned)ceil_div(tpi, SI_LW), (unsigned)n), SI_LW * 32, 0, st>>>(
+            x_dense, c, h, w, tiles_x, tpi, ctr, s.cap_slots, ts, slots);
+        rc = check_launch("si_tile_lists_dense_kernel");
+    } else {
+        si_tile_lists_kernel<TY, TX><<<dim3((unsigned)ceil_div(tpi, SI_LW), (unsigned)n), SI_LW * 32, 0, st>>>(
+            nodes, seg_off, n_nodes, n, c, h, w, tiles_x, tpi, ctr, s.cap_slots, ts, slots);
+        rc = check_launch("si_tile_lists_kernel");
+    }
     if (rc == FSCNN_OK) {
         dim3 grid((unsigned)ceil_div(s.n_tiles, NW), (unsigned)(kp / (64 * PAIRS)));
         si3x3_tl_kernel<TY, TX, PAIRS, NW, MINB><<<grid, NW * 32, 0, st>>>(
@@ -696,6 +779,23 @@ int fscnn_si_conv3x3_fast_pool(const fscnn_node *in_nodes, const int64_t *in_seg
     }
     // one filter per lane (K < 64)
     return launch_fast<4, 8, 2, 1>(nd, in_seg_off, n_nodes, n, c, h, w, wf, k, g.kp, bias, y, st, pool);
+}
+
+int fscnn_si_conv3x3_fast_dense(const float *x, int n, int c, int h, int w, const float *wf, int k,
+                                const float *bias, int pool, float *y, void *stream) {
+    FSCNN_REQUIRE(pool >= 0 && pool <= 2, "pool must be 0 (none), 1 (2x2 max) or 2 (2x2 avg)");
+    if (pool) FSCNN_REQUIRE(h % 2 == 0 && w % 2 == 0, "fused 2x2 pool needs even extents");
+    FSCNN_REQUIRE(n >= 0 && c > 0 && h > 0 && w > 0 && k >= 0, "bad extents");
+    if (n == 0 || k == 0) return FSCNN_OK;
+    FSCNN_REQUIRE(x && wf && y, "null buffer");
+    FSCNN_REQUIRE(n <= 65535, "batch too large for one launch (%d > 65535)", n);
+    const SiGeom g = si_fast_geom(k);
+    FSCNN_REQUIRE(g.kt >= 2, "the dense-input path needs K >= 64 (got %d)", k);
+    FSCNN_REQUIRE(n * (int64_t)ceil_div(w, 4) * ceil_div(h, 4) < (1ll << 31), "too many tiles");
+    cudaStream_t st = as_stream(stream);
+    if (g.kt == 2)
+        return launch_tl<4, 8, 1, 4, 5>(nullptr, nullptr, 0, n, c, h, w, wf, k, g.kp, bias, y, st, pool, x);
+    return launch_tl<4, 4, 2, 4, 4>(nullptr, nullptr, 0, n, c, h, w, wf, k, g.kp, bias, y, st, pool, x);
 }
 
 int fscnn_si_conv3x3_fast(const fscnn_node *in_nodes, const int64_t *in_seg_off, int64_t n_nodes, int n,

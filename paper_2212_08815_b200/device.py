@@ -526,6 +526,21 @@ def si_conv3x3_fast(nodes: torch.Tensor, seg_off: torch.Tensor, n: int, c: int, 
     return out
 
 
+def si_conv3x3_fast_dense(x: torch.Tensor, wf: torch.Tensor, k: int, bias: torch.Tensor | None = None,
+                          out: torch.Tensor | None = None, pool: str | None = None) -> torch.Tensor:
+    """si_conv3x3_fast straight from a dense [n, c, h, w] activation: bit-identical to
+    encoding x in CHW order and calling si_conv3x3_fast (same tile streams), without
+    the encode (and its host sync) between sparse-input layers.  K >= 64."""
+    x = x.contiguous()
+    n, c, h, w = (int(v) for v in x.shape)
+    mode = {None: 0, "max": 1, "avg": 2}[pool]
+    if out is None:
+        shape = (n, k, h // 2, w // 2) if mode else (n, k, h, w)
+        out = torch.empty(shape, dtype=torch.float32, device=x.device)
+    call("fscnn_si_conv3x3_fast_dense", ptr(x), n, c, h, w, ptr(wf), k, ptr(bias), mode, ptr(out), stream())
+    return out
+
+
 # -- dense layers / layout ----------------------------------------------------------------
 
 

@@ -582,7 +582,6 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
             geom = ConvGeometry(dims, (c_f, h_f, w_f), step.stride, step.padding)
             bias = _step_bias(step, dev)
             if sparse:
-                enc = device.encode_order(x, "CHW")
                 _, ci, hi, wi = (int(v) for v in x.shape)
                 fused = False
                 if (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1) and not ly._EXACT and \
@@ -592,14 +591,17 @@ def _forward_batched(prepared: PreparedNet, batch, densities=None) -> list:
                     if step.fused_pool is not None and tuple(step.fused_pool) == (2, 2) and hi % 2 == 0 \
                             and wi % 2 == 0:
                         fp = "max" if step.fused_pool_mode == ly.POOL_MAX else "avg"
-                    y = device.si_conv3x3_fast(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "fast"), k,
-                                               pool=fp)
+                    # straight from the dense activation: the same tile streams as encoding it
+                    # (bit-identical), without the encode and its host sync
+                    y = device.si_conv3x3_fast_dense(x, _step_bank(step, "fast"), k, pool=fp)
                     fused = fp is not None
-                elif (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
-                    y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "strip"), k)
                 else:
-                    y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "gather"), k, h_f,
-                                       w_f, step.stride, step.padding)
+                    enc = device.encode_order(x, "CHW")
+                    if (h_f, w_f, step.stride, step.padding) == (3, 3, 1, 1):
+                        y = device.si_conv3x3(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "strip"), k)
+                    else:
+                        y = device.si_conv(enc.nodes, enc.seg_off, n, ci, hi, wi, _step_bank(step, "gather"), k,
+                                           h_f, w_f, step.stride, step.padding)
                 if step.fused_pool is not None and not fused:
                     h_p, w_p = ly._pool_args(step.fused_pool, step.fused_pool_mode, geom.n_h, geom.n_w)
                     y = device.pool2d(y, h_p, w_p, step.fused_pool_mode == ly.POOL_MAX)

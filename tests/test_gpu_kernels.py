@@ -512,3 +512,26 @@ def test_si_fast_fused_pool_equals_conv_then_pool(dev, mode):
         got = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, wf, k, bias=_t(b), pool=mode)
         assert tuple(got.shape) == (n, k, h // 2, w // 2)
         assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (n, c, k, h, w)
+
+
+@pytest.mark.parametrize("k,pool", [(64, None), (96, "max"), (128, None), (256, "avg"), (130, "max")])
+def test_si_fast_dense_input_equals_node_input(dev, k, pool):
+    """fscnn_si_conv3x3_fast_dense (tile streams straight from a dense activation) is bit
+    for bit the node-input kernel on the encoded activation: +-0.0 not stored, NaN and
+    inf stored, ragged tiles, several images."""
+    rng = np.random.default_rng(k)
+    n, c, h, w = 3, 40, 18, 22
+    x = np.abs(rng.standard_normal((n, c, h, w))).astype(np.float32)
+    x[rng.random(x.shape) < 0.6] = 0
+    x[0, 1, 2, 3] = -0.0
+    x[1, 5, 0, 0] = np.nan
+    x[2, 7, 17, 21] = np.inf
+    x[2, 8, 4, 4] = -1.5
+    wt = rng.standard_normal((k, c, 3, 3)).astype(np.float32)
+    bias = rng.standard_normal(k).astype(np.float32)
+    xd = _t(x)
+    wf = dev.si_pack_fast(_t(wt))
+    enc = dev.encode_order(xd, "CHW")
+    ref = dev.si_conv3x3_fast(enc.nodes, enc.seg_off, n, c, h, w, wf, k, _t(bias), pool=pool).cpu().numpy()
+    got = dev.si_conv3x3_fast_dense(xd, wf, k, _t(bias), pool=pool).cpu().numpy()
+    assert np.array_equal(got.view(np.int32), ref.view(np.int32))
