@@ -441,10 +441,10 @@ def _pinned(key: str, nbytes: int):
 
 def _upload_sparse_batch(batch, c: int, h: int, w: int, dev):
     """The batch's CHW node tensors as one device node buffer + global segment offsets
-    (packed into pinned staging, one H2D each), or None when a stored node has value
-    +-0.0 (checked on the device: the dense batched path cannot represent it)."""
-    import torch
-
+    (packed into pinned staging on host threads, one H2D each), or None -- the caller
+    then takes the per-image path -- when a stored node has value +-0.0 (the dense
+    batched path cannot represent it) or the structure is not the reference format's
+    (both checked on the device)."""
     with _pinned_lock:  # the staging is reused: held until the copies have completed
         return _upload_sparse_batch_locked(batch, c, h, w, dev)
 
