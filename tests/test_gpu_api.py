@@ -347,7 +347,7 @@ def test_full_size_config5_batch_invariance(oracle):
 # -- batch-sharded multi-process stack (distributed.ShardedVGG) ----------------------
 
 
-def _sharded_worker(rank, world, port, layers, xs, q):
+def _sharded_worker(rank, world, port, layers, xs, q, backend="gloo"):
     import os
 
     import torch
@@ -357,7 +357,10 @@ def _sharded_worker(rank, world, port, layers, xs, q):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)  # both ranks share the one GPU: gloo carries the collectives
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         sh = pd.ShardedVGG(layers if rank == 0 else None, hw=32, device=torch.device("cuda", 0))
         outs, secs = sh.timed_forward([fs.DenseTensor3.from_array(a) for a in xs])
@@ -405,3 +408,38 @@ def test_sharded_forward_byte_identical_world2():
         assert outs == ref, r
         assert full == ref_dev, r
         assert timed
+
+
+def test_sharded_forward_nccl_world1():
+    """The same SPMD flow with the production backend: NCCL collectives on device buffers
+    (bank broadcast of the int32 node pairs / int64 offset tables / f32 bias, the padded
+    rank-ordered all-gather, the max-over-ranks reduce).  One GPU is reachable, so the
+    NCCL group has one rank; the outputs must equal the plain single-GPU forward byte for
+    byte."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2212_08815_b200.engine import VGGEngine
+
+    layers = wl.vgg16_weights(seed=23, zero_frac=0.9, scale=0.125)
+    rng = np.random.default_rng(24)
+    xs = [rng.standard_normal((3, 32, 32)).astype(np.float32) for _ in range(3)]
+    eng = VGGEngine(layers, batch=3, hw=32)
+    prepared = nw.prepared_from_engine(eng)
+    ref = [o.data.tobytes() for o in fs.forward(prepared, [fs.DenseTensor3.from_array(a) for a in xs]).outputs]
+    ref_dev = eng.forward_device(torch.from_numpy(np.stack(xs)).cuda()).contiguous().cpu().numpy().tobytes()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_sharded_worker, args=(0, 1, port, layers, xs, q, "nccl"))
+    p.start()
+    _, outs, full, timed = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert outs == ref
+    assert full == ref_dev
+    assert timed
