@@ -124,6 +124,22 @@ def fp32_peak_tflops(torch, lib):
     return best, nominal
 
 
+def host_threads(oracle) -> int:
+    """Threads for the CPU arm: every core this process may run on.  torchrun exports
+    OMP_NUM_THREADS=1 to its ranks when the variable is unset, which would silently make
+    the N>1 reference arm single-threaded -- the count is passed to the oracle explicitly
+    (omp_set_num_threads) unless the caller chose one with FSCNN_CPU_THREADS."""
+    if not oracle.max_threads() or oracle.lib().oracle_has_openmp() == 0:
+        return 1
+    env = os.environ.get("FSCNN_CPU_THREADS")
+    if env:
+        return max(1, int(env))
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
 def cpu_baseline(layers, hw, sample_images, budget_s=12.0, seed=2024):
     """Oracle port of the reference CPU path on this host, all cores; images/s."""
     from oracle import oracle
@@ -133,17 +149,27 @@ def cpu_baseline(layers, hw, sample_images, budget_s=12.0, seed=2024):
     for wt, b in layers:
         nodes, seg = oracle.encode_bank(wt)
         banks.append((nodes, seg, wt.shape[0], b))
-    threads = oracle.max_threads()
+    threads = host_threads(oracle)
     x = wl.vgg16_input(1, seed=seed, hw=hw)
-    oracle.vgg_forward(x, banks)  # warm (page-in)
+    oracle.vgg_forward(x, banks, threads)  # warm (page-in)
     done, t0 = 0, time.perf_counter()
     while done < sample_images and (done == 0 or time.perf_counter() - t0 < budget_s):
-        oracle.vgg_forward(x, banks)
+        oracle.vgg_forward(x, banks, threads)
         done += 1
     dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "images/s", "cores": threads, "kind": "port",
             "sample": f"{done} image(s) of the same workload (batch-1 forwards), {dt:.1f} s, oracle/ C port "
                       "of the reference numba kernels (strategy-II arithmetic), OpenMP over output pixels"}
+
+
+def bench_config(desc, n_total, world, backend, zf):
+    """The line's ``config`` object -- the same for both arms (the reference arm times a
+    bounded sample of this workload, described in its ``cpu_baseline.sample``)."""
+    return {"workload": desc, "global_batch": n_total, "seq_len": None,
+            "parallelism": f"dp{world} (batch-sharded, filters broadcast once)",
+            "collectives": backend if world > 1 else None,
+            "filter_zero_fraction": zf,
+            "l2": "working set > L2 (activations 0.4 GB per layer at batch 32)"}
 
 
 def run_reference(args):
@@ -161,24 +187,28 @@ def run_reference(args):
         nodes, seg = oracle.encode_bank(wt)
         banks.append((nodes, seg, wt.shape[0], b))
     x = wl.vgg16_input(1, seed=104)
+    threads = host_threads(oracle)
     for _ in range(args.warmup):
-        oracle.vgg_forward(x, banks)
+        oracle.vgg_forward(x, banks, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.vgg_forward(x, banks)
+        oracle.vgg_forward(x, banks, threads)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded numpy, workloads.py)",
-        "config": {"workload": desc, "sample": "1 image per step", "global_batch": 1, "seq_len": None,
-                   "parallelism": "cpu-openmp"},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": oracle.max_threads(), "kind": "port",
-                         "sample": "1 image per step through the oracle/ C port of the reference kernels"},
+        "higher_is_better": True, "scaling": "weak" if args.workload == "c3" else "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded numpy, workloads.py): x~N(0,1), W~N(0,sqrt(2/fan_in)) i.i.d. masked",
+        "config": bench_config(desc, batch * args.gpus if args.workload == "c3" else batch, args.gpus,
+                               os.environ.get("FSCNN_DIST_BACKEND", "nccl"), zf),
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": "1 image of the workload per step (the reference forwards images one by one: "
+                                   "batch-1 forwards, OpenMP over output pixels) through the oracle/ C port of "
+                                   "the reference kernels, on rank 0's host cores"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -433,11 +463,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.workload == "c3" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded numpy, workloads.py): x~N(0,1), W~N(0,sqrt(2/fan_in)) i.i.d. masked",
-            "config": {"workload": desc, "global_batch": n_total, "seq_len": None,
-                       "parallelism": f"dp{world} (batch-sharded, filters broadcast once)",
-                       "collectives": backend if world > 1 else None,
-                       "filter_zero_fraction": zf,
-                       "l2": "working set > L2 (activations 0.4 GB per layer at batch 32)"},
+            "config": bench_config(desc, n_total, world, backend, zf),
             "nnz_gflops": flops_img * n_total * args.steps / (elapsed_ms * 1e-3) / 1e9,
             "nnz_gflop_per_image": flops_img / 1e9,
             "roofline": {"bound": "fp32",
