@@ -83,12 +83,23 @@ def comm_device(device: torch.device, group=None) -> torch.device:
     return device if dist.get_backend(group) == "nccl" else torch.device("cpu")
 
 
-def gather_batch(y_local: torch.Tensor, total: int, group=None) -> torch.Tensor:
+def gather_batch(y_local: torch.Tensor, total: int, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """Rank-ordered all-gather of per-rank batch shards [n_r, ...] (n_r from shard_range,
-    possibly unequal) into the full [total, ...] batch on every rank."""
+    possibly unequal) into the full [total, ...] batch on every rank.
+
+    Equal shards on the collective's own device (NCCL, total % world == 0 -- every bench
+    configuration) are ONE collective straight into ``out`` (or a fresh tensor): no
+    padding, no staging copies, no concatenation.  Unequal shards are padded to the
+    largest one and trimmed after the gather."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     lo, hi = shard_range(total, rank, world)
     assert int(y_local.shape[0]) == hi - lo
+    if total % world == 0 and comm_device(y_local.device, group) == y_local.device and y_local.is_contiguous():
+        shape = (total,) + tuple(y_local.shape[1:])
+        if out is None or tuple(out.shape) != shape or out.dtype != y_local.dtype or out.device != y_local.device:
+            out = torch.empty(shape, dtype=y_local.dtype, device=y_local.device)
+        dist.all_gather_into_tensor(out, y_local, group=group)
+        return out
     n_max = shard_range(total, 0, world)[1]  # rank 0 holds the largest shard
     dev = comm_device(y_local.device, group)
     pad = torch.zeros((n_max,) + tuple(y_local.shape[1:]), dtype=y_local.dtype, device=dev)
@@ -164,7 +175,10 @@ class ShardedVGG:
         output [total, 512, H/32, W/32] on every rank."""
         total = int(x.shape[0]) * self.world if total is None else total
         y = self.engine.forward_device_dense(x)
-        return gather_batch(y, total, self.group)
+        # equal shards gather into one reused buffer (valid until the next call, like the
+        # engine's own output buffers)
+        self._full = gather_batch(y, total, self.group, out=getattr(self, "_full", None))
+        return self._full
 
     def forward(self, batch: list, dst: int | None = None) -> list | None:
         """network.forward for the batch-sharded stack: host DenseTensor3 list in (the same

@@ -210,7 +210,13 @@ def _dist_worker(rank, world, port, q):
         # unequal shards (5 items over 2 ranks: 3 + 2) gathered in rank order
         a, b = pd.shard_range(5, rank, world)
         full = pd.gather_batch(torch.arange(a, b, dtype=torch.float32).repeat_interleave(4).view(b - a, 2, 2), 5)
-        q.put((rank, sig, (lo, hi), gathered, mx, full.numpy().tolist(), str(pd.comm_device(dev))))
+        # equal shards (6 over 2): the single-collective path, into a caller-owned buffer
+        a, b = pd.shard_range(6, rank, world)
+        buf = torch.full((6, 2, 2), -1.0)
+        eq = pd.gather_batch(torch.arange(a, b, dtype=torch.float32).repeat_interleave(4).view(b - a, 2, 2), 6, out=buf)
+        assert eq.data_ptr() == buf.data_ptr()
+        q.put((rank, sig, (lo, hi), gathered, mx, full.numpy().tolist(), str(pd.comm_device(dev)),
+               eq.numpy().tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -239,6 +245,7 @@ def test_batch_sharded_driver_gloo_world2():
     want = [[[float(i)] * 2] * 2 for i in range(5)]
     assert res[0][4] == res[1][4] == want
     assert res[0][5] == "cpu"
+    assert res[0][6] == res[1][6] == [[[float(i)] * 2] * 2 for i in range(6)]
 
 
 def test_shard_range_covers_batch():
