@@ -354,15 +354,35 @@ def main():
             cur = out
             w = w // 2 if st.pool else w
     peak_meas, peak_nom = fp32_peak_tflops(torch, _lib)
-    # DRAM traffic per layer of the dominant kernel, from the committed ncu summary of this
-    # same command (profiles/r02_bench_traffic.json), when present
-    traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r02_bench_traffic.json" if jit_on else "r01_bench_launches_summary.json")
-    if os.path.exists(prof) and args.workload == "c3":
-        with open(prof) as fh:
-            d = json.load(fh)
-        traffic = d.get("dram_bytes_per_layer", d.get("sf3x3_dram_bytes_per_launch"))
-        traffic_src = f"profiles/{os.path.basename(prof)} (ncu, cold cache)"
+    # DRAM traffic per layer of the dominant kernel from the committed ncu summaries of this
+    # step: the whole CUDA graph profiled as one workload (profiles/r02_graph_traffic.json:
+    # kernels concurrent, L2 shared, as timed here) and, beside it, the serialised
+    # cold-cache launch list (profiles/r02_bench_traffic.json: every group kernel of a
+    # layer re-reads the layer's input from DRAM there)
+    traffic, traffic_src, traffic_serial = None, None, None
+
+    def _prof(name):
+        path = os.path.join(ROOT, "profiles", name)
+        if not (os.path.exists(path) and args.workload == "c3"):
+            return None
+        with open(path) as fh:
+            return json.load(fh)
+
+    if jit_on:
+        d = _prof("r02_bench_traffic.json")
+        if d:
+            traffic_serial = d.get("dram_bytes_per_layer")
+            traffic, traffic_src = traffic_serial, "profiles/r02_bench_traffic.json (ncu launch list, serialised, cold cache)"
+        d = _prof("r02_graph_traffic.json")
+        if d:
+            traffic = d["dram_bytes_per_layer"]
+            traffic_src = ("profiles/r02_graph_traffic.json (ncu --graph-profiling graph --cache-control none: "
+                           "the step's CUDA graph as one workload, total DRAM bytes / 13 layers)")
+    else:
+        d = _prof("r01_bench_launches_summary.json")
+        if d:
+            traffic = d.get("sf3x3_dram_bytes_per_launch")
+            traffic_src = "profiles/r01_bench_launches_summary.json (ncu, cold cache)"
     kern_ms = sum(layer_ms)
     per_launch_tf = flops_img * n_local / (kern_ms * 1e-3) / 1e12
     # the dominant kernel family is ~100 % of the step's kernel time (ncu launch list,
@@ -484,6 +504,7 @@ def main():
                          "hbm_gbs_peak": peaks.get("hbm_gbs"),
                          "achieved_hbm_gbs": eng.bytes_per_image() * n_local / (kern_ms * 1e-3) / 1e9,
                          "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
+                         "traffic_serialised_cold": traffic_serial,
                          "algorithmic_bytes_per_launch": eng.bytes_per_image() * n_local / len(eng.steps),
                          "per_layer_ms": [round(v, 4) for v in layer_ms]},
             "gpu_launches": launches,
