@@ -380,8 +380,15 @@ def _engine_device_forward(prepared: PreparedNet, batch):
         np_in = h_in.numpy().reshape(n, elems)
 
         def fill(lo, hi):
-            for i in range(lo, hi):
+            # on host threads (numpy copies release the GIL)
+            def pack(i):
                 np_in[i] = batch[i].data
+
+            if hi - lo > 1:
+                list(_pack_pool().map(pack, range(lo, hi)))
+            else:
+                for i in range(lo, hi):
+                    pack(i)
 
         src = h_in
     if ly._EXACT:  # set_exact(True): the reference-order kernels, bit-exact
