@@ -172,6 +172,7 @@ struct Plan {
     int tma_hint;  // 1: input boxes loaded L2 evict-first
     int store_cs;  // 1: outputs stored streaming (evict-first)
     int nobar;     // 1: per-stage empty mbarriers instead of a CTA barrier per chunk
+    int tma_split; // TMA operations per box (each CC / tma_split channels; they run concurrently)
 };
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -290,6 +291,12 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     }
     p.CC = std::min(p.CC, c);
     p.S = std::min<int>(p.S, (c + p.CC - 1) / p.CC);  // no stages beyond the chunks
+    // one box as tma_split TMA operations of CC / tma_split channels each (same bytes, same
+    // layout: the channel is the box's outermost extent); FSCNN_SFJIT_TMA_SPLIT requests it,
+    // the largest divisor of CC not above the request is taken
+    p.tma_split = getenv("FSCNN_SFJIT_TMA_SPLIT") ? std::max(1, atoi(getenv("FSCNN_SFJIT_TMA_SPLIT"))) : 1;
+    p.tma_split = std::min(p.tma_split, p.CC);
+    while (p.CC % p.tma_split || (((int64_t)p.CC / p.tma_split) * per_ch) % 128) --p.tma_split;
     p.box_bytes = align_up((int64_t)p.CC * per_ch, 128);
     p.stage_bytes = p.NB * p.box_bytes;
     p.smem_bytes = p.S * p.stage_bytes + 16 * p.S;  // full[S] + empty[S] mbarriers
@@ -451,13 +458,22 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
         o("add.u32 q2, rbar, %d;", 8 * s);
         o("mov.u32 q3, 0;");
         o("%sISS%d:", lp.c_str(), j);
-        if (p.tma_hint)
-            o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [qdst], "
-              "[tm, {q3, qy, qc, qimg}], [q2], pol;");
-        else
-            o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [qdst], [tm, "
-              "{q3, qy, qc, qimg}], [q2];");
-        o("add.u32 qdst, qdst, %lld;", (long long)p.box_bytes);
+        const int cs = p.CC / p.tma_split;
+        const long long sub_bytes = (long long)cs * p.BH * p.P * 4;
+        for (int sub = 0; sub < p.tma_split; ++sub) {
+            if (sub) {
+                o("add.u32 qc, qc, %d;", cs);
+                o("add.u32 qdst, qdst, %lld;", sub_bytes);
+            }
+            if (p.tma_hint)
+                o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [qdst], "
+                  "[tm, {q3, qy, qc, qimg}], [q2], pol;");
+            else
+                o("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [qdst], [tm, "
+                  "{q3, qy, qc, qimg}], [q2];");
+        }
+        if (p.tma_split > 1) o("mov.u32 qc, %d;", c0);
+        o("add.u32 qdst, qdst, %lld;", (long long)p.box_bytes - (p.tma_split - 1) * sub_bytes);
         o("add.u32 qimg, qimg, 1;");
         o("mov.u32 qy, -1;");
         o("add.u32 qbi, qbi, 1;");
@@ -886,7 +902,7 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
     if (x != j->map_x || n != j->map_n || ldi != j->map_ldi) {
         cuuint64_t gdim[4] = {(cuuint64_t)p.W + 1, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)n};
         cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * p.H * 4, (cuuint64_t)ldi * p.H * p.C * 4};
-        cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)p.CC, 1};
+        cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)(p.CC / p.tma_split), 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         r = d.encodeTiled(&j->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride, box,
                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
