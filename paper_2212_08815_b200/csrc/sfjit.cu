@@ -173,6 +173,7 @@ struct Plan {
     int store_cs;  // 1: outputs stored streaming (evict-first)
     int nobar;     // 1: per-stage empty mbarriers instead of a CTA barrier per chunk
     int tma_split; // TMA operations per box (each CC / tma_split channels; they run concurrently)
+    int tma_merge; // 1: whole-image mode loads a chunk's Q image boxes as ONE operation (box image extent Q)
 };
 
 int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -296,8 +297,14 @@ bool make_plan(Plan &p, int c, int k, int h, int w, int relu, int pool, int flag
     // the largest divisor of CC not above the request is taken
     p.tma_split = getenv("FSCNN_SFJIT_TMA_SPLIT") ? std::max(1, atoi(getenv("FSCNN_SFJIT_TMA_SPLIT"))) : 1;
     p.tma_split = std::min(p.tma_split, p.CC);
-    while (p.CC % p.tma_split || (((int64_t)p.CC / p.tma_split) * per_ch) % 128) --p.tma_split;
+    while (p.tma_split > 1 && (p.CC % p.tma_split || (((int64_t)p.CC / p.tma_split) * per_ch) % 128)) --p.tma_split;
     p.box_bytes = align_up((int64_t)p.CC * per_ch, 128);
+    // whole-image CTAs: the Q images' boxes of a chunk as one TMA operation (the image is
+    // the box's outermost extent, images past the batch are zero-filled and counted)
+    // (one operation instead of Q per chunk: VGG16 14x14 layers -3..-10 %, C3 step +0.7 %,
+    // bit-identical; FSCNN_SFJIT_TMA_MERGE=0 keeps one operation per image)
+    p.tma_merge = !(getenv("FSCNN_SFJIT_TMA_MERGE") && !atoi(getenv("FSCNN_SFJIT_TMA_MERGE"))) && p.MODE == 1 && p.NB > 1 &&
+                  p.tma_split == 1 && p.box_bytes == (int64_t)p.CC * per_ch;
     p.stage_bytes = p.NB * p.box_bytes;
     p.smem_bytes = p.S * p.stage_bytes + 16 * p.S;  // full[S] + empty[S] mbarriers
     if (p.smem_bytes > 227 * 1024) {
@@ -447,7 +454,10 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
         const int c0 = j * p.CC;
         // the transaction count is the bytes the boxes deliver (boxes sit at 128-byte
         // aligned strides, but only CC*BH*P floats of each are written)
-        o("mul.lo.u32 q0, nbox, %lld;", (long long)p.CC * p.BH * p.P * 4);
+        if (p.tma_merge)
+            o("mov.u32 q0, %lld;", (long long)p.NB * p.CC * p.BH * p.P * 4);
+        else
+            o("mul.lo.u32 q0, nbox, %lld;", (long long)p.CC * p.BH * p.P * 4);
         o("mbarrier.arrive.expect_tx.shared::cta.b64 _, [rbar+%d], q0;", 8 * s);
         o("mov.u32 qdst, smem;");
         o("add.u32 qdst, qdst, %lld;", (long long)(s * p.stage_bytes));
@@ -477,7 +487,10 @@ std::string gen_kernel(const Plan &p, const float *wt, const float *bias, int g_
         o("add.u32 qimg, qimg, 1;");
         o("mov.u32 qy, -1;");
         o("add.u32 qbi, qbi, 1;");
-        o("setp.lt.u32 pl, qbi, nbox;");
+        if (p.tma_merge)
+            o("setp.lt.u32 pl, qbi, 1;");
+        else
+            o("setp.lt.u32 pl, qbi, nbox;");
         o("@pl bra %sISS%d;", lp.c_str(), j);
     };
     for (int j = 0; j < std::min(p.S, p.n_chunks); ++j) issue(j);
@@ -902,7 +915,7 @@ int fscnn_sfjit_launch(fscnn_sfjit *j, const float *x, int n, int ldi, float *y,
     if (x != j->map_x || n != j->map_n || ldi != j->map_ldi) {
         cuuint64_t gdim[4] = {(cuuint64_t)p.W + 1, (cuuint64_t)p.H, (cuuint64_t)p.C, (cuuint64_t)n};
         cuuint64_t gstride[3] = {(cuuint64_t)ldi * 4, (cuuint64_t)ldi * p.H * 4, (cuuint64_t)ldi * p.H * p.C * 4};
-        cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)(p.CC / p.tma_split), 1};
+        cuuint32_t box[4] = {(cuuint32_t)p.P, (cuuint32_t)p.BH, (cuuint32_t)(p.CC / p.tma_split), (cuuint32_t)(p.tma_merge ? p.NB : 1)};
         cuuint32_t es[4] = {1, 1, 1, 1};
         r = d.encodeTiled(&j->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(x), gdim, gstride, box,
                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
