@@ -327,6 +327,21 @@ def test_sfjit_generator_emits_valid_ptx_and_compiles():
         finally:
             del os.environ["FSCNN_JIT_CACHE"]
             lib.fscnn_sfjit_destroy(h_)
+    # every VGG16 conv shape plans and generates (C = 3: a box that is not a 128-byte
+    # multiple; 14x14: whole-image CTAs whose chunk is ONE TMA operation over 4 images)
+    for c, k, h, pool in ((3, 64, 224, 0), (64, 64, 224, 1), (64, 128, 112, 0), (128, 256, 56, 0),
+                          (256, 512, 28, 0), (512, 512, 28, 1), (512, 512, 14, 0), (512, 512, 14, 1)):
+        w = (rng.standard_normal((k, c, 3, 3)) * 0.1).astype(np.float32)
+        w[rng.random(w.shape) < 0.9] = 0
+        b = np.zeros(k, np.float32)
+        n = lib.fscnn_sfjit_ptx(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 48, 0, None, 0)
+        assert n > 0, (c, k, h, lib.fscnn_last_error())
+        if h == 14:
+            buf = ctypes.create_string_buffer(n + 1)
+            lib.fscnn_sfjit_ptx(w.ctypes.data, b.ctypes.data, k, c, h, h, 1, pool, 48, 0, buf, n + 1)
+            text = buf.value.decode()
+            # one TMA per chunk: the issue loop runs once (not once per image)
+            assert "setp.lt.u32 pl, qbi, 1;" in text and "setp.lt.u32 pl, qbi, nbox;" not in text
     # odd extents are refused with a message (the engine then keeps the jump-table kernel)
     w = np.ones((8, 4, 3, 3), np.float32)
     assert lib.fscnn_sfjit_ptx(w.ctypes.data, None, 8, 4, 15, 15, 1, 0, 0, 0, None, 0) == -1
