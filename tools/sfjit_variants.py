@@ -28,7 +28,7 @@ for spec in sys.argv[2:]:
     name, _, kv = spec.partition(":")
     env = dict(item.split("=", 1) for item in kv.split(",") if item)
     variants.append((name, env))
-KEYS = ("KT", "WMAX", "SMEM_KB", "MINB", "ODD", "NOBAR", "TMA_HINT", "STORE_CS", "REPEAT", "PADTPR", "TMA_SPLIT", "REALP", "TMA_MERGE")
+KEYS = ("KT", "WMAX", "SMEM_KB", "MINB", "ODD", "NOBAR", "TMA_HINT", "STORE_CS", "REPEAT", "PADTPR", "TMA_SPLIT", "REALP", "TMA_MERGE", "UNI")
 
 
 def time_fn(fn):
